@@ -1,0 +1,164 @@
+/*
+ * rl_cddt.h — C ABI of the B200-native CDDT range method, beam sensor model
+ * and particle-filter step.
+ *
+ * This is the drop-in boundary for the reference's range-method path
+ * (rangelib, /root/reference/proj). Every entry point names the reference
+ * interface it replaces (file:line relative to the reference tree). Plain
+ * pointers and sizes only: no C++ or torch types cross this boundary, no
+ * exceptions escape it. INTEGRATION.md shows the reference-side adapter
+ * (a rangelib::RangeMethod subclass) and the ctypes binding.
+ *
+ * Conventions
+ *  - Geometry is in pixel units, angles in radians counter-clockwise from +x,
+ *    cell (x, y) at y * width + x (proj/include/rangelib/grid.hpp:12-16).
+ *  - theta_disc is the number of discrete directions over the full circle,
+ *    even and >= 4 (RangeMethodConfig, proj/include/rangelib/raycast.hpp:51-64).
+ *  - Functions suffixed _batch take DEVICE pointers and run asynchronously on
+ *    `stream` (a cudaStream_t; NULL = the handle's own stream, in which case
+ *    the call also synchronises before returning). _host variants take host
+ *    pointers and return when the results are in host memory.
+ *  - Status codes mirror the reference's exceptions; the message of the last
+ *    failure on the calling thread is available from rl_last_error().
+ */
+#ifndef RL_CDDT_H
+#define RL_CDDT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RL_OK 0
+#define RL_EINVAL 1      /* std::invalid_argument (bad theta_disc / max_range / sizes) */
+#define RL_ELOGIC 2      /* std::logic_error: edit after prune (cddt.cpp:333) */
+#define RL_ERANGE 3      /* std::out_of_range: edit outside the grid (cddt.cpp:334) */
+#define RL_ECUDA 4       /* CUDA runtime failure */
+#define RL_ENOMEM 5      /* device or host allocation failure */
+#define RL_EDEGENERATE 6 /* sensor_update returned false: weights reset to uniform (mcl.cpp:114-117) */
+#define RL_EPARSE 7      /* ParseError on a snapshot (cddt.cpp:502-579) */
+
+typedef struct rl_cddt rl_cddt;
+
+typedef struct {
+  int32_t width, height, theta_disc, slice_count;
+  int32_t pruned, device;
+  double max_range, resolution;
+  uint64_t rows;         /* bin rows over all slices (sum of SliceProjection::bin_count) */
+  uint64_t zero_points;  /* Cddt::zero_point_count (cddt.hpp:193) */
+  uint64_t memory_bytes; /* Cddt::memory_bytes accounting (cddt.hpp:200-203) */
+  uint64_t device_bytes; /* bytes actually resident on the device for the structure */
+  double init_seconds;   /* wall-clock build time, as make_method records (methods.cpp:118-133) */
+} rl_cddt_info_t;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *rl_last_error(void);
+
+/* Cddt::Cddt (proj/src/cddt.cpp:136-171) + Cddt::prune (cddt.cpp:281-330) when
+ * prune != 0, i.e. make_method(cddt | pcddt, grid, cfg) (methods.cpp:118-133).
+ * grid: width*height bytes, nonzero = occupied (host memory). max_range 0 =
+ * grid diagonal (raycast.hpp:61-63). device: CUDA ordinal the structure lives on. */
+int rl_cddt_create(const uint8_t *grid, int32_t width, int32_t height, double resolution,
+                   int32_t theta_disc, double max_range, int32_t prune, int32_t device,
+                   rl_cddt **out);
+int rl_cddt_destroy(rl_cddt *c);
+
+/* Cddt::prune (cddt.cpp:281-330). Idempotent. */
+int rl_cddt_prune(rl_cddt *c);
+
+int rl_cddt_info(const rl_cddt *c, rl_cddt_info_t *out);
+
+/* Cddt::cast (cddt.cpp:271-273) / RangeMethod::cast (methods.hpp:27). */
+int rl_cddt_cast(rl_cddt *c, double x, double y, double theta, double *out);
+
+/* Cddt::cast_pair (cddt.cpp:275-279): ranges at theta and theta + pi. */
+int rl_cddt_cast_pair(rl_cddt *c, double x, double y, double theta, double *out_fwd,
+                      double *out_bwd);
+
+/* Batched Cddt::cast over f32 queries (the batched replacement for the
+ * per-query loop of run_batches, proj/src/bench.cpp:86-106). Device pointers.
+ * hit_cell (optional): y*width+x of the occupied cell that settled the answer,
+ * -1 when the result is max_range without a hit. */
+int rl_cddt_cast_batch(rl_cddt *c, const float *x, const float *y, const float *theta,
+                       float *out, int32_t *hit_cell, size_t n, void *stream);
+
+/* Same in f64 (x, y, theta widened exactly), with the resolving zero point
+ * (global row, index in row) as the reference's MarkSink sees it
+ * (cddt.cpp:249, :259). Any of out/hit_cell/res_row/res_idx may be NULL. */
+int rl_cddt_cast_batch_f64(rl_cddt *c, const double *x, const double *y, const double *theta,
+                           double *out, int32_t *hit_cell, int64_t *res_row, int32_t *res_idx,
+                           size_t n, void *stream);
+
+/* Cddt::directional_cast (cddt.cpp:207-269) at explicit direction indices. */
+int rl_cddt_directional_batch(rl_cddt *c, const double *x, const double *y, const int32_t *a,
+                              double *out, size_t n, void *stream);
+
+/* Host-memory batched casts: host -> device copies, kernel and device -> host
+ * copies pipelined in chunks over several streams. Pinned host buffers give
+ * full PCIe bandwidth; pageable ones work but copy slower. */
+int rl_cddt_cast_batch_host(rl_cddt *c, const float *x, const float *y, const float *theta,
+                            float *out, size_t n);
+
+/* Cddt::set_occupancy (cddt.cpp:332-377). */
+int rl_cddt_set_occupancy(rl_cddt *c, int32_t x, int32_t y, int32_t occupied);
+
+/* n edits applied in order with set_occupancy semantics; xy = n (x, y) pairs,
+ * occupied = n flags (host memory). The structure afterwards equals a fresh
+ * build of the edited grid (proj/tests/test_cddt.cpp:578-604). If edit k is
+ * outside the grid, edits [0, k) are applied and RL_ERANGE is returned, as a
+ * loop of set_occupancy calls would leave it. */
+int rl_cddt_set_occupancy_batch(rl_cddt *c, const int32_t *xy, const uint8_t *occupied,
+                                size_t n);
+
+/* Copy the structure to host memory (any pointer may be NULL):
+ *   slice_row_base[slice_count+1]  global row index of (slice, 0)
+ *   row_off[rows+1]                CSR offsets into zp
+ *   zp[zero_points]                concatenation of Cddt::bin(s, r).values()
+ *   membership[w*h], grid[w*h]     0/1 bytes */
+int rl_cddt_export(const rl_cddt *c, uint32_t *slice_row_base, uint64_t *row_off, float *zp,
+                   uint8_t *membership, uint8_t *grid);
+
+/* Snapshot I/O in the reference's binary format (serialize_cddt /
+ * deserialize_cddt, cddt.cpp:458-579). rl_cddt_serialize writes at most cap
+ * bytes and stores the full size in *size (call with buf NULL to query). */
+int rl_cddt_serialize(const rl_cddt *c, uint8_t *buf, size_t cap, size_t *size);
+int rl_cddt_deserialize(const uint8_t *buf, size_t n, int32_t device, rl_cddt **out);
+
+/* Wait for all work queued on the handle's stream. */
+int rl_cddt_sync(rl_cddt *c);
+
+/* ---- beam sensor model and particle filter (proj/src/mcl.cpp) ---- */
+
+/* BeamModelParams (proj/include/rangelib/mcl.hpp:32-40). */
+typedef struct {
+  double w_hit, w_short, w_max, w_rand, sigma_hit, lambda_short, z_max;
+} rl_beam_params_t;
+
+/* beam_likelihood (mcl.cpp:11-40) on the host, for building tables. */
+double rl_beam_likelihood(const rl_beam_params_t *p, double expected, double measured);
+
+/* Discretised likelihood table T[m][e] = float(beam_likelihood(e/inv_res,
+ * m/inv_res)) for e, m in [0, zdim), written to host memory. */
+int rl_beam_table(const rl_beam_params_t *p, int32_t zdim, double inv_res, float *table);
+
+/* sensor_update (mcl.cpp:58-120), fused on the GPU: per particle, nbeams casts
+ * at theta + beam_offset(b) (ScanSpec, mcl.hpp:42-51), likelihood per beam,
+ * FP64 log-sum, max-subtract, exp, normalise. Device pointers:
+ *   px, py, pt [n]  particle poses (f64, as rangelib::Particle, mcl.hpp:11-16)
+ *   scan [nbeams]   measured ranges (f64)
+ *   table           NULL = analytic beam_likelihood with *params; otherwise
+ *                   zdim*zdim f32 T[m][e] indexed by clamp(iround(r*inv_res))
+ *   logw, weight [n] outputs (f64); either may be NULL.
+ * Returns RL_EDEGENERATE (weights set to 1/n) where the reference returns false. */
+int rl_sensor_update(rl_cddt *c, const double *px, const double *py, const double *pt, size_t n,
+                     const double *scan, int32_t nbeams, double fov, const rl_beam_params_t *params,
+                     const float *table, int32_t zdim, double inv_res, double *logw, double *weight,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RL_CDDT_H */

@@ -1,0 +1,108 @@
+"""ctypes binding of the C ABI in include/rl_cddt.h.
+
+The library is the only compute path: if librl_cddt.so is missing the import
+fails loudly (there is no CPU fallback). Build it with
+``python -m paper_1705_01167_b200.build`` or ``__graft_entry__.build()``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "librl_cddt.so"
+
+RL_OK, RL_EINVAL, RL_ELOGIC, RL_ERANGE, RL_ECUDA, RL_ENOMEM, RL_EDEGENERATE, RL_EPARSE = range(8)
+
+
+class ParseError(ValueError):
+    """rangelib::ParseError (proj/include/rangelib/grid.hpp:81-90)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (edits after prune, proj/src/cddt.cpp:333)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class rl_cddt_info_t(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32), ("height", C.c_int32), ("theta_disc", C.c_int32),
+        ("slice_count", C.c_int32), ("pruned", C.c_int32), ("device", C.c_int32),
+        ("max_range", C.c_double), ("resolution", C.c_double), ("rows", C.c_uint64),
+        ("zero_points", C.c_uint64), ("memory_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
+        ("init_seconds", C.c_double),
+    ]
+
+
+class rl_beam_params_t(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("w_hit", "w_short", "w_max", "w_rand", "sigma_hit", "lambda_short", "z_max")]
+
+
+_P = C.c_void_p
+_SIG = {
+    "rl_last_error": (C.c_char_p, []),
+    "rl_cddt_create": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double,
+                                 C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rl_cddt_destroy": (C.c_int, [_P]),
+    "rl_cddt_prune": (C.c_int, [_P]),
+    "rl_cddt_info": (C.c_int, [_P, C.POINTER(rl_cddt_info_t)]),
+    "rl_cddt_cast": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
+    "rl_cddt_cast_pair": (C.c_int, [_P, C.c_double, C.c_double, C.c_double,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "rl_cddt_cast_batch": (C.c_int, [_P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "rl_cddt_cast_batch_f64": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "rl_cddt_directional_batch": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "rl_cddt_cast_batch_host": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t]),
+    "rl_cddt_set_occupancy": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32]),
+    "rl_cddt_set_occupancy_batch": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "rl_cddt_export": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "rl_cddt_serialize": (C.c_int, [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "rl_cddt_deserialize": (C.c_int, [_P, C.c_size_t, C.c_int32, C.POINTER(_P)]),
+    "rl_cddt_sync": (C.c_int, [_P]),
+    "rl_beam_likelihood": (C.c_double, [C.POINTER(rl_beam_params_t), C.c_double, C.c_double]),
+    "rl_beam_table": (C.c_int, [C.POINTER(rl_beam_params_t), C.c_int32, C.c_double, _P]),
+    "rl_sensor_update": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,
+                                   C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double, _P,
+                                   _P, _P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load librl_cddt.so (once). Raises ImportError when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -m paper_1705_01167_b200.build); there is no CPU fallback")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIG.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+def check(status: int) -> int:
+    """Map a status code to the reference's exception types."""
+    if status in (RL_OK, RL_EDEGENERATE):
+        return status
+    msg = lib().rl_last_error().decode(errors="replace")
+    if status == RL_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if status == RL_ELOGIC:
+        raise LogicError(msg)
+    if status == RL_ERANGE:
+        raise IndexError(msg)  # std::out_of_range
+    if status == RL_EPARSE:
+        raise ParseError(msg)
+    if status == RL_ENOMEM:
+        raise MemoryError(msg)
+    raise CudaError(msg or f"status {status}")

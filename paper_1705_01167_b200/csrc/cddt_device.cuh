@@ -1,0 +1,232 @@
+// Device-side CDDT query: the exact FP64 restatement of Cddt::directional_cast
+// (proj/src/cddt.cpp:207-269) and detail::RayWalker
+// (proj/include/rangelib/detail/ray_walker.hpp:21-104) for sm_100a.
+//
+// Bit-exactness contract: every TU including this header is
+// compiled with -fmad=false so no FP64 multiply-add is contracted; the
+// direction lattice cos/sin comes from the host (glibc) and is uploaded;
+// division, floor, ceil, fmod and conversions are IEEE-exact on the device.
+#pragma once
+
+#include <cstdint>
+
+namespace rl {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // raycast.hpp:12
+constexpr double kNearField = 0.75;                           // cddt.cpp:19
+constexpr double kVerifyHalf = 0.7072;                        // cddt.cpp:25
+constexpr double kLatticeEps = 1e-9;                          // cddt.cpp:26
+constexpr double kWalkNone = -1.0;                            // ray_walker.hpp:23
+constexpr double kWalkExit = -2.0;                            // ray_walker.hpp:24
+
+// per-cell flag byte
+constexpr uint8_t kOcc = 1;     // occupied
+constexpr uint8_t kClear = 2;   // cell and all in-bounds 8-neighbours free (cddt.cpp:173-180)
+constexpr uint8_t kMember = 4;  // edge cell with stored zero points (grid.cpp:110-119)
+
+// Per-slice projection (SliceProjection, cddt.hpp:22-33) packed for one
+// 32-byte load: cos, sin, y_offset, bin_count, global row base.
+struct __align__(32) SliceParam {
+  double cos_t, sin_t, y_offset;
+  int32_t bin_count;
+  uint32_t row_base;
+};
+
+// Read-only view of one device-resident structure, passed by value.
+struct CddtView {
+  const uint8_t* __restrict__ flags;      // w*h
+  const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
+  const float* __restrict__ zp;           // zero points, ascending per row
+  const SliceParam* __restrict__ slices;  // S
+  const double2* __restrict__ dirs;       // K (cos, sin), axis-snapped (cddt.cpp:30-42)
+  int w, h, K, S;
+  double max_range;
+};
+
+__host__ __device__ __forceinline__ double fmin_std(double a, double b) { return (b < a) ? b : a; }
+__host__ __device__ __forceinline__ double fmax_std(double a, double b) { return (a < b) ? b : a; }
+
+__device__ __forceinline__ long iround(double v) { return (long)ceil(v - 0.5); }  // raycast.hpp:17
+
+__device__ __forceinline__ double normalize_angle_2pi(double t) {  // raycast.hpp:20-25
+  t = fmod(t, kTwoPi);
+  if (t < 0) t += kTwoPi;
+  if (t >= kTwoPi) t = 0.0;
+  return t;
+}
+
+__device__ __forceinline__ int direction_index(double theta, int K) {  // raycast.hpp:36-40
+  long i = iround(theta * (double)K / kTwoPi) % K;
+  if (i < 0) i += K;
+  return (int)i;
+}
+
+__device__ __forceinline__ bool occ_at(const CddtView& c, int x, int y) {
+  return (__ldg(c.flags + (size_t)y * c.w + x) & kOcc) != 0;
+}
+__device__ __forceinline__ bool in_bounds(const CddtView& c, int x, int y) {
+  return x >= 0 && x < c.w && y >= 0 && y < c.h;
+}
+
+__device__ __forceinline__ double boundary_t(double d, double o, int cc) {  // ray_walker.hpp:75-79
+  if (d > 0) return ((double)cc + 1.0 - o) / d;
+  if (d < 0) return ((double)cc - o) / d;
+  return __longlong_as_double(0x7ff0000000000000ll);
+}
+
+struct Walker {
+  double ox, oy, dx, dy, t, tnx, tny;
+  int cx, cy;
+
+  __device__ __forceinline__ void place(double tt) {  // ray_walker.hpp:62-73
+    t = tt;
+    double px = ox + tt * dx, py = oy + tt * dy;
+    cx = (int)floor(px);
+    cy = (int)floor(py);
+    if (dx < 0 && px == (double)cx) cx--;
+    if (dy < 0 && py == (double)cy) cy--;
+    tnx = boundary_t(dx, ox, cx);
+    tny = boundary_t(dy, oy, cy);
+  }
+  __device__ __forceinline__ void init(double x, double y, double ddx, double ddy) {
+    ox = x;
+    oy = y;
+    dx = ddx;
+    dy = ddy;
+    place(0.0);
+  }
+  __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
+    if (tt > t) place(tt);
+  }
+  __device__ __forceinline__ void advance() {  // ray_walker.hpp:81-97
+    if (tnx == tny) {
+      t = tnx;
+      cx += dx > 0 ? 1 : -1;
+      cy += dy > 0 ? 1 : -1;
+      tnx = boundary_t(dx, ox, cx);
+      tny = boundary_t(dy, oy, cy);
+    } else if (tnx < tny) {
+      t = tnx;
+      cx += dx > 0 ? 1 : -1;
+      tnx = boundary_t(dx, ox, cx);
+    } else {
+      t = tny;
+      cy += dy > 0 ? 1 : -1;
+      tny = boundary_t(dy, oy, cy);
+    }
+  }
+  __device__ __forceinline__ double scan_to(const CddtView& c, double lim) {  // :51-59
+    for (;;) {
+      if (!in_bounds(c, cx, cy)) return kWalkExit;
+      if (occ_at(c, cx, cy)) return t;
+      double tn = tnx < tny ? tnx : tny;
+      if (tn > lim) return kWalkNone;
+      advance();
+    }
+  }
+};
+
+// Outcome of one query beyond the range: the occupied cell that settled it
+// and the resolving zero point (what MarkSink::mark receives, cddt.cpp:249,259).
+struct CastOut {
+  int32_t hit;      // y*w+x or -1
+  uint32_t res_g;   // global row of the resolving zero point
+  int32_t res_idx;  // index within the row, -1 when no zero point resolved
+};
+
+// Cddt::directional_cast (cddt.cpp:207-269).
+__device__ __forceinline__ double directional_cast(const CddtView& c, double x, double y, int a,
+                                                   CastOut& o) {
+  o.hit = -1;
+  o.res_idx = -1;
+  o.res_g = 0;
+  const int cxi = (int)floor(x), cyi = (int)floor(y);
+  if (!in_bounds(c, cxi, cyi)) return c.max_range;
+  const uint8_t f0 = __ldg(c.flags + (size_t)cyi * c.w + cxi);
+  if (f0 & kOcc) {
+    o.hit = cyi * c.w + cxi;
+    return 0.0;
+  }
+  const bool forward = a < c.S;
+  const int s = forward ? a : a - c.S;
+  const SliceParam sp = c.slices[s];
+  const double xq = x * sp.cos_t + y * sp.sin_t;                 // cddt.hpp:31
+  const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;  // cddt.hpp:32
+  int row = (int)yq;
+  if (row < 0) row = 0;
+  if (row >= sp.bin_count) row = sp.bin_count - 1;
+  const double2 dir = __ldg(c.dirs + a);
+  const double dx = dir.x, dy = dir.y;
+
+  Walker wk;
+  bool have_walker = false;
+  if (!(f0 & kClear)) {
+    wk.init(x, y, dx, dy);
+    have_walker = true;
+    double r = wk.scan_to(c, kNearField);
+    if (r >= 0.0) {
+      o.hit = wk.cy * c.w + wk.cx;
+      return (c.max_range < r) ? c.max_range : r;
+    }
+    if (r == kWalkExit) return c.max_range;
+  }
+
+  double result = c.max_range;
+  const double gw = (double)c.w, gh = (double)c.h;
+  const uint32_t g = sp.row_base + (uint32_t)row;
+  const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
+  const float* __restrict__ v = c.zp + lo;
+  // std::upper_bound (forward, xq < double(v)) / std::lower_bound (backward,
+  // double(v) < xq) with libstdc++'s halving sequence (cddt.hpp:106-131)
+  uint32_t first = 0, len = hi - lo;
+  while (len > 0) {
+    uint32_t half = len >> 1, mid = first + half;
+    double vm = (double)__ldg(v + mid);
+    bool right = forward ? !(xq < vm) : (vm < xq);
+    if (right) {
+      first = mid + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  const int n = (int)(hi - lo);
+  int idx = forward ? (int)first : (int)first - 1;
+  const int step = forward ? 1 : -1;
+  for (; idx >= 0 && idx < n; idx += step) {
+    const double vv = (double)__ldg(v + idx);
+    const double d = forward ? vv - xq : xq - vv;
+    if (d >= c.max_range) break;
+    // landing-cell probe (cddt.cpp:239-253)
+    const double px = x + d * dx, py = y + d * dy;
+    if (px >= 0.0 && py >= 0.0 && px < gw && py < gh) {
+      const int hx = (int)px, hy = (int)py;
+      const double fx = px - (double)hx, fy = py - (double)hy;
+      if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
+          fy < 1.0 - kLatticeEps && occ_at(c, hx, hy)) {
+        o.hit = hy * c.w + hx;
+        o.res_g = g;
+        o.res_idx = idx;
+        result = d;
+        break;
+      }
+    }
+    // verification window around the candidate (cddt.cpp:254-261)
+    if (!have_walker) {
+      wk.init(x, y, dx, dy);
+      have_walker = true;
+    }
+    wk.seek(d - kVerifyHalf);
+    double r = wk.scan_to(c, d + kVerifyHalf);
+    if (r == kWalkExit) break;
+    if (r < 0.0) continue;
+    o.hit = wk.cy * c.w + wk.cx;
+    o.res_g = g;
+    o.res_idx = idx;
+    result = d;
+    break;
+  }
+  return result;
+}
+
+}  // namespace rl

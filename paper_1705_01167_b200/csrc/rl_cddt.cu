@@ -1,0 +1,699 @@
+// CDDT / PCDDT construction, pruning and batched queries on sm_100a, behind
+// the C ABI in include/rl_cddt.h.
+//
+// Device layout:
+//   flags[w*h]      u8  bit0 occupied, bit1 clear-3x3, bit2 membership
+//   row_off[rows+1] u32 CSR offsets, rows = sum over slices of bin_count,
+//                       slice s owns global rows [row_base[s], row_base[s]+bin_count)
+//   zp[zero_points] f32 zero points, ascending within each row
+//   slices[S]       SliceParam (cos, sin, y_offset, bin_count, row_base)
+//   dirs[K]         double2 direction lattice, host glibc cos/sin, axis snapped
+//
+// Construction (Cddt::Cddt, proj/src/cddt.cpp:136-171) is a count -> scan ->
+// scatter -> segmented sort pipeline; pruning (cddt.cpp:281-330) is a marking
+// pass of K casts per free cell followed by a stream compaction.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "rl_common.cuh"
+
+namespace rl {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int finish(const rl_cddt* c, void* s) {
+  RL_CK(cudaGetLastError());
+  if (!s) RL_CK(cudaStreamSynchronize(c->stream));
+  return RL_OK;
+}
+
+// direction_components (cddt.cpp:30-42), host glibc.
+static void direction_components(int i, int K, double* c, double* s) {
+  long long q4 = 4LL * i;
+  if (q4 % K == 0) {
+    int q = int(q4 / K) & 3;
+    *c = (q == 0) ? 1.0 : (q == 2) ? -1.0 : 0.0;
+    *s = (q == 1) ? 1.0 : (q == 3) ? -1.0 : 0.0;
+  } else {
+    double t = double(i) * kTwoPi / double(K);
+    *c = std::cos(t);
+    *s = std::sin(t);
+  }
+}
+
+static inline double smin(double a, double b) { return (b < a) ? b : a; }  // std::min
+static inline double smax(double a, double b) { return (a < b) ? b : a; }  // std::max
+
+// Direction tables and slice projections (SliceProjection::make, cddt.cpp:44-60).
+int init_geometry(rl_cddt* c) {
+  c->S = c->K / 2;
+  c->dcos.resize(c->K);
+  c->dsin.resize(c->K);
+  for (int a = 0; a < c->K; a++) direction_components(a, c->K, &c->dcos[a], &c->dsin[a]);
+  c->slices.resize(c->S);
+  uint64_t base = 0;
+  for (int s = 0; s < c->S; s++) {
+    double sn = c->dsin[s], cs = c->dcos[s];
+    double A = 0.0, B = -double(c->w) * sn, C = double(c->h) * cs, D = B + C;
+    double lo = smin(smin(A, B), smin(C, D)), hi = smax(smax(A, B), smax(C, D));
+    SliceParam& p = c->slices[s];
+    p.cos_t = cs;
+    p.sin_t = sn;
+    p.y_offset = -lo;
+    p.bin_count = int(std::ceil(hi - lo)) + 1;
+    p.row_base = uint32_t(base);
+    base += uint64_t(p.bin_count);
+  }
+  if (base >= (1ull << 31)) {
+    set_error("cddt: %llu bin rows exceed the 32-bit row index", (unsigned long long)base);
+    return RL_EINVAL;
+  }
+  c->rows = base;
+  RL_TRY(c->d_slices.alloc(c->S));
+  RL_TRY(c->d_dirs.alloc(c->K));
+  std::vector<double2> dirs(c->K);
+  for (int a = 0; a < c->K; a++) dirs[a] = make_double2(c->dcos[a], c->dsin[a]);
+  RL_CK(cudaMemcpyAsync(c->d_slices.p, c->slices.data(), sizeof(SliceParam) * c->S,
+                        cudaMemcpyHostToDevice, c->stream));
+  RL_CK(cudaMemcpyAsync(c->d_dirs.p, dirs.data(), sizeof(double2) * c->K, cudaMemcpyHostToDevice,
+                        c->stream));
+  RL_CK(cudaStreamSynchronize(c->stream));
+  return RL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K1: per-cell flags. occupied; clear = cell and all in-bounds 8-neighbours
+// free (clear_around, cddt.cpp:173-180); member = occupied with a free or
+// out-of-bounds 8-neighbour (is_edge_cell, grid.cpp:110-119).
+__global__ void k_flags(const uint8_t* __restrict__ grid, uint8_t* __restrict__ flags, int w,
+                        int h) {
+  const size_t n = size_t(w) * h;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int x = int(i % w), y = int(i / w);
+    const bool occ = grid[i] != 0;
+    bool any_occ_nb = false, any_free_or_oob_nb = false;
+    for (int dy = -1; dy <= 1; dy++)
+      for (int dx = -1; dx <= 1; dx++) {
+        if (dx == 0 && dy == 0) continue;
+        int nx = x + dx, ny = y + dy;
+        if (nx < 0 || ny < 0 || nx >= w || ny >= h) {
+          any_free_or_oob_nb = true;
+        } else if (grid[size_t(ny) * w + nx]) {
+          any_occ_nb = true;
+        } else {
+          any_free_or_oob_nb = true;
+        }
+      }
+    uint8_t f = 0;
+    if (occ) f |= kOcc;
+    if (!occ && !any_occ_nb) f |= kClear;
+    if (occ && any_free_or_oob_nb) f |= kMember;
+    flags[i] = f;
+  }
+}
+
+// Compact member cells into an (unordered) edge list; warp-aggregated atomics.
+__global__ void k_edge_list(const uint8_t* __restrict__ flags, size_t n, int32_t* __restrict__ edges,
+                            unsigned int* __restrict__ count) {
+  for (size_t base = blockIdx.x * size_t(blockDim.x); base < n;
+       base += size_t(gridDim.x) * blockDim.x) {
+    size_t i = base + threadIdx.x;
+    bool m = i < n && (flags[i] & kMember);
+    unsigned ballot = __ballot_sync(0xffffffffu, m);
+    unsigned lane = threadIdx.x & 31;
+    unsigned pos0 = 0;
+    if (lane == 0 && ballot) pos0 = atomicAdd(count, __popc(ballot));
+    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+    if (m) edges[pos0 + __popc(ballot & ((1u << lane) - 1))] = int32_t(i);
+  }
+}
+
+// for_each_bin_of_pixel (cddt.cpp:118-134): rows [r0, r1] of slice sp whose
+// unit strip overlaps pixel (px, py) with positive area, and the pixel
+// centre's projected x' rounded to f32.
+__device__ __forceinline__ void pixel_rows(const SliceParam& sp, int px, int py, int& r0, int& r1,
+                                           float& v) {
+  auto py_of = [&](double x, double y) { return -x * sp.sin_t + y * sp.cos_t + sp.y_offset; };
+  double c0 = py_of(double(px), double(py));
+  double c1 = py_of(double(px + 1), double(py));
+  double c2 = py_of(double(px), double(py + 1));
+  double c3 = py_of(double(px + 1), double(py + 1));
+  double lo = fmin_std(fmin_std(c0, c1), fmin_std(c2, c3));
+  double hi = fmax_std(fmax_std(c0, c1), fmax_std(c2, c3));
+  r0 = int(floor(lo));
+  r1 = int(ceil(hi)) - 1;
+  if (r0 < 0) r0 = 0;
+  if (r1 >= sp.bin_count) r1 = sp.bin_count - 1;
+  const double cx = double(px) + 0.5, cy = double(py) + 0.5;
+  v = __double2float_rn(cx * sp.cos_t + cy * sp.sin_t);
+}
+
+// K2a/K2b: per (edge pixel, slice): count rows, then scatter values.
+template <bool SCATTER>
+__global__ void k_points(const int32_t* __restrict__ edges, unsigned n_edges,
+                         const SliceParam* __restrict__ slices, int S, int w,
+                         uint32_t* __restrict__ cnt, const uint32_t* __restrict__ row_off,
+                         float* __restrict__ zp) {
+  const uint64_t total = uint64_t(n_edges) * S;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const unsigned e = unsigned(i / S);
+    const int s = int(i % S);
+    const int32_t cell = edges[e];
+    const int px = cell % w, py = cell / w;
+    const SliceParam sp = slices[s];
+    int r0, r1;
+    float v;
+    pixel_rows(sp, px, py, r0, r1, v);
+    for (int r = r0; r <= r1; r++) {
+      const uint32_t g = sp.row_base + uint32_t(r);
+      if (SCATTER) {
+        uint32_t pos = row_off[g] + atomicAdd(&cnt[g], 1u);
+        zp[pos] = v;
+      } else {
+        atomicAdd(&cnt[g], 1u);
+      }
+    }
+  }
+}
+
+struct ToU64 {
+  __host__ __device__ unsigned long long operator()(uint32_t v) const { return v; }
+};
+
+static int grid_blocks(size_t work, int threads) {
+  size_t b = (work + threads - 1) / threads;
+  size_t cap = size_t(sm_count()) * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return int(b);
+}
+
+// Full construction from c->grid_h: flags, membership mirror, CSR.
+int build_structure(rl_cddt* c) {
+  const size_t wh = size_t(c->w) * c->h;
+  cudaStream_t st = c->stream;
+  DevBuf<uint8_t> d_grid;
+  RL_TRY(d_grid.alloc(wh));
+  RL_TRY(c->flags.alloc(wh));
+  RL_CK(cudaMemcpyAsync(d_grid.p, c->grid_h.data(), wh, cudaMemcpyHostToDevice, st));
+  k_flags<<<grid_blocks(wh, 256), 256, 0, st>>>(d_grid.p, c->flags.p, c->w, c->h);
+  RL_CK(cudaGetLastError());
+
+  DevBuf<int32_t> edges;
+  DevBuf<unsigned> d_count;
+  RL_TRY(edges.alloc(wh));
+  RL_TRY(d_count.alloc(1));
+  RL_CK(cudaMemsetAsync(d_count.p, 0, sizeof(unsigned), st));
+  k_edge_list<<<grid_blocks(wh, 256), 256, 0, st>>>(c->flags.p, wh, edges.p, d_count.p);
+  unsigned n_edges = 0;
+  RL_CK(cudaMemcpyAsync(&n_edges, d_count.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+
+  const uint64_t rows = c->rows;
+  DevBuf<uint32_t> cnt;
+  RL_TRY(cnt.alloc(rows + 1));
+  RL_TRY(c->row_off.alloc(rows + 1));
+  RL_CK(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * (rows + 1), st));
+  const uint64_t pairs = uint64_t(n_edges) * c->S;
+  if (pairs)
+    k_points<false><<<grid_blocks(pairs, 256), 256, 0, st>>>(edges.p, n_edges, c->d_slices.p,
+                                                             c->S, c->w, cnt.p, nullptr, nullptr);
+  RL_CK(cudaGetLastError());
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.p, c->row_off.p, int(rows + 1), st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt.p, c->row_off.p, int(rows + 1), st));
+  }
+  uint64_t total = 0;
+  {
+    // 64-bit total so a wrapped 32-bit CSR offset is detected, not silently used
+    DevBuf<unsigned long long> d_total;
+    RL_TRY(d_total.alloc(1));
+    auto wide = cub::TransformInputIterator<unsigned long long, ToU64, const uint32_t*>(cnt.p, ToU64());
+    size_t tmp_bytes = 0;
+    cub::DeviceReduce::Sum(nullptr, tmp_bytes, wide, d_total.p, int(rows), st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceReduce::Sum(tmp.p, tmp_bytes, wide, d_total.p, int(rows), st));
+    RL_CK(cudaMemcpyAsync(&total, d_total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    RL_CK(cudaStreamSynchronize(st));
+  }
+  if (total >= (1ull << 31)) {
+    set_error("cddt: %llu zero points exceed the 31-bit CSR offset", (unsigned long long)total);
+    return RL_EINVAL;
+  }
+  c->zero_points = total;
+
+  DevBuf<float> unsorted;
+  RL_TRY(unsorted.alloc(total));
+  RL_TRY(c->zp.alloc(total));
+  RL_CK(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * (rows + 1), st));
+  if (pairs)
+    k_points<true><<<grid_blocks(pairs, 256), 256, 0, st>>>(edges.p, n_edges, c->d_slices.p, c->S,
+                                                            c->w, cnt.p, c->row_off.p, unsorted.p);
+  RL_CK(cudaGetLastError());
+  if (total) {
+    size_t tmp_bytes = 0;
+    cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, unsorted.p, c->zp.p, int(total),
+                                       int(rows), c->row_off.p, c->row_off.p + 1, st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, unsorted.p, c->zp.p, int(total),
+                                             int(rows), c->row_off.p, c->row_off.p + 1, st));
+  }
+  // host membership mirror
+  c->member_h.assign(wh, 0);
+  {
+    std::vector<uint8_t> fl(wh);
+    RL_CK(cudaMemcpyAsync(fl.data(), c->flags.p, wh, cudaMemcpyDeviceToHost, st));
+    RL_CK(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < wh; i++) c->member_h[i] = (fl[i] & kMember) ? 1 : 0;
+  }
+  return RL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K3: batched casts, one thread per query, grid-stride.
+template <class T>
+__global__ void __launch_bounds__(256) k_cast(CddtView c, const T* __restrict__ qx,
+                                              const T* __restrict__ qy, const T* __restrict__ qt,
+                                              T* __restrict__ out, int32_t* __restrict__ hit,
+                                              int64_t* __restrict__ res_row,
+                                              int32_t* __restrict__ res_idx, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double x = double(qx[i]), y = double(qy[i]);
+    const double th = normalize_angle_2pi(double(qt[i]));  // RayQuery ctor, raycast.hpp:47
+    const int a = direction_index(th, c.K);
+    CastOut o;
+    const double r = directional_cast(c, x, y, a, o);
+    if (out) out[i] = T(r);
+    if (hit) hit[i] = o.hit;
+    if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
+    if (res_idx) res_idx[i] = o.res_idx;
+  }
+}
+
+__global__ void k_directional(CddtView c, const double* __restrict__ x,
+                              const double* __restrict__ y, const int32_t* __restrict__ a,
+                              double* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    CastOut o;
+    out[i] = directional_cast(c, x[i], y[i], a[i], o);
+  }
+}
+
+__global__ void k_single(CddtView c, double x, double y, double theta, int pair,
+                         double* __restrict__ out) {
+  const double th = normalize_angle_2pi(theta);
+  const int a = direction_index(th, c.K);
+  CastOut o;
+  out[0] = directional_cast(c, x, y, a, o);
+  if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
+}
+
+static int cast_blocks(size_t n) {
+  // enough resident warps to cover the dependent-load latency; grid-stride beyond
+  size_t b = (n + 255) / 256;
+  size_t cap = size_t(sm_count()) * 8;
+  return int(std::max<size_t>(1, std::min(b, cap)));
+}
+
+// ---------------------------------------------------------------------------
+// K4: prune marking. One state per (free cell centre, direction); the
+// resolving index and its near-side neighbour are marked (cddt.cpp:289-299).
+__global__ void __launch_bounds__(256) k_prune_mark(CddtView c, uint8_t* __restrict__ marks) {
+  const uint64_t total = uint64_t(c.w) * c.h * c.K;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t cell = i / c.K;
+    const int a = int(i % c.K);
+    if (__ldg(c.flags + cell) & kOcc) continue;  // occupied origins never consult bins
+    const int cx = int(cell % c.w), cy = int(cell / c.w);
+    CastOut o;
+    directional_cast(c, double(cx) + 0.5, double(cy) + 0.5, a, o);
+    if (o.res_idx < 0) continue;
+    const uint32_t lo = c.row_off[o.res_g], n = c.row_off[o.res_g + 1] - lo;
+    uint8_t* m = marks + lo;
+    m[o.res_idx] = 1;
+    if (a < c.S) {
+      if (o.res_idx > 0) m[o.res_idx - 1] = 1;
+    } else {
+      if (uint32_t(o.res_idx) + 1 < n) m[o.res_idx + 1] = 1;
+    }
+  }
+}
+
+__global__ void k_widen(const uint8_t* __restrict__ in, uint32_t* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i <= n;
+       i += size_t(gridDim.x) * blockDim.x)
+    out[i] = i < n ? uint32_t(in[i]) : 0u;
+}
+
+__global__ void k_compact(const float* __restrict__ zp, const uint8_t* __restrict__ marks,
+                          const uint32_t* __restrict__ pos, float* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    if (marks[i]) out[pos[i]] = zp[i];
+}
+
+__global__ void k_remap_offsets(const uint32_t* __restrict__ old_off,
+                                const uint32_t* __restrict__ pos, uint32_t* __restrict__ new_off,
+                                size_t rows) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
+       g += size_t(gridDim.x) * blockDim.x)
+    new_off[g] = pos[old_off[g]];
+}
+
+int prune_structure(rl_cddt* c) {
+  if (c->pruned) return RL_OK;
+  cudaStream_t st = c->stream;
+  const size_t n = c->zero_points;
+  DevBuf<uint8_t> marks;
+  RL_TRY(marks.alloc(n));
+  RL_CK(cudaMemsetAsync(marks.p, 0, n ? n : 1, st));
+  const uint64_t states = uint64_t(c->w) * c->h * c->K;
+  k_prune_mark<<<int(std::max<uint64_t>(1, std::min<uint64_t>((states + 255) / 256,
+                                                                 uint64_t(sm_count()) * 8))),
+                 256, 0, st>>>(c->view(), marks.p);
+  RL_CK(cudaGetLastError());
+  DevBuf<uint32_t> wide, pos;
+  RL_TRY(wide.alloc(n + 1));
+  RL_TRY(pos.alloc(n + 1));
+  k_widen<<<grid_blocks(n + 1, 256), 256, 0, st>>>(marks.p, wide.p, n);
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, wide.p, pos.p, int(n + 1), st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, wide.p, pos.p, int(n + 1), st));
+  }
+  uint32_t kept = 0;
+  RL_CK(cudaMemcpyAsync(&kept, pos.p + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+  DevBuf<float> nzp;
+  DevBuf<uint32_t> noff;
+  RL_TRY(nzp.alloc(kept));
+  RL_TRY(noff.alloc(c->rows + 1));
+  k_compact<<<grid_blocks(n, 256), 256, 0, st>>>(c->zp.p, marks.p, pos.p, nzp.p, n);
+  k_remap_offsets<<<grid_blocks(c->rows + 1, 256), 256, 0, st>>>(c->row_off.p, pos.p, noff.p,
+                                                                  c->rows);
+  RL_CK(cudaGetLastError());
+  RL_CK(cudaStreamSynchronize(st));
+  c->zp = std::move(nzp);
+  c->row_off = std::move(noff);
+  c->zero_points = kept;
+  c->pruned = true;
+  return RL_OK;
+}
+
+int create_handle(int32_t device, rl_cddt** out, rl_cddt** keep) {
+  *out = nullptr;
+  int ndev = 0;
+  RL_CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("cddt: device %d not available (%d devices)", device, ndev);
+    return RL_EINVAL;
+  }
+  rl_cddt* c = new rl_cddt();
+  c->dev = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    set_error("cudaStreamCreate: %s", cudaGetErrorString(e));
+    return RL_ECUDA;
+  }
+  *keep = c;
+  return RL_OK;
+}
+
+}  // namespace rl
+
+using namespace rl;
+
+extern "C" {
+
+const char* rl_last_error(void) { return g_err.c_str(); }
+
+int rl_cddt_create(const uint8_t* grid, int32_t width, int32_t height, double resolution,
+                   int32_t theta_disc, double max_range, int32_t prune, int32_t device,
+                   rl_cddt** out) {
+  if (!out) return RL_EINVAL;
+  *out = nullptr;
+  if (!grid || width <= 0 || height <= 0) {
+    set_error("grid dimensions must be positive");  // grid.hpp:21
+    return RL_EINVAL;
+  }
+  if (!(resolution > 0.0)) {
+    set_error("resolution must be positive");  // grid.hpp:22
+    return RL_EINVAL;
+  }
+  if (max_range < 0.0) {
+    set_error("max_range must be >= 0");  // raycast.hpp:56
+    return RL_EINVAL;
+  }
+  if (theta_disc < 4 || theta_disc % 2 != 0) {
+    set_error("theta_disc must be even and >= 4");  // raycast.hpp:57-58
+    return RL_EINVAL;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  DeviceGuard guard(device);
+  rl_cddt* c = nullptr;
+  RL_TRY(create_handle(device, out, &c));
+  c->w = width;
+  c->h = height;
+  c->K = theta_disc;
+  c->resolution = resolution;
+  c->max_range = max_range > 0.0 ? max_range
+                                 : std::sqrt(double(width) * width + double(height) * height);
+  const size_t wh = size_t(width) * height;
+  c->grid_h.resize(wh);
+  for (size_t i = 0; i < wh; i++) c->grid_h[i] = grid[i] ? 1 : 0;
+  int st = init_geometry(c);
+  if (st == RL_OK) st = build_structure(c);
+  if (st == RL_OK && prune) st = prune_structure(c);
+  if (st != RL_OK) {
+    std::string msg = g_err;
+    rl_cddt_destroy(c);
+    g_err = msg;
+    return st;
+  }
+  c->init_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = c;
+  return RL_OK;
+}
+
+int rl_cddt_destroy(rl_cddt* c) {
+  if (!c) return RL_OK;
+  {
+    DeviceGuard guard(c->dev);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->flags.release();
+    c->row_off.release();
+    c->zp.release();
+    c->d_slices.release();
+    c->d_dirs.release();
+    c->d_scalar.release();
+    c->ws.release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+  }
+  delete c;
+  return RL_OK;
+}
+
+int rl_cddt_prune(rl_cddt* c) {
+  if (!c) return RL_EINVAL;
+  DeviceGuard guard(c->dev);
+  return prune_structure(c);
+}
+
+int rl_cddt_info(const rl_cddt* c, rl_cddt_info_t* o) {
+  if (!c || !o) return RL_EINVAL;
+  o->width = c->w;
+  o->height = c->h;
+  o->theta_disc = c->K;
+  o->slice_count = c->S;
+  o->pruned = c->pruned;
+  o->device = c->dev;
+  o->max_range = c->max_range;
+  o->resolution = c->resolution;
+  o->rows = c->rows;
+  o->zero_points = c->zero_points;
+  const uint64_t wh = uint64_t(c->w) * c->h;
+  o->memory_bytes = 4 * c->zero_points + (wh + 7) / 8 + uint64_t(c->S) * 48;  // cddt.hpp:200-203
+  o->device_bytes = c->flags.bytes() + c->row_off.bytes() + 4 * c->zero_points +
+                    c->d_slices.bytes() + c->d_dirs.bytes();
+  o->init_seconds = c->init_seconds;
+  return RL_OK;
+}
+
+int rl_cddt_sync(rl_cddt* c) {
+  if (!c) return RL_EINVAL;
+  DeviceGuard guard(c->dev);
+  RL_CK(cudaStreamSynchronize(c->stream));
+  return RL_OK;
+}
+
+static int single(rl_cddt* c, double x, double y, double theta, int pair, double* o0,
+                  double* o1) {
+  DeviceGuard guard(c->dev);
+  if (!c->d_scalar.p) RL_TRY(c->d_scalar.alloc(2));
+  k_single<<<1, 1, 0, c->stream>>>(c->view(), x, y, theta, pair, c->d_scalar.p);
+  RL_CK(cudaGetLastError());
+  double r[2];
+  RL_CK(cudaMemcpyAsync(r, c->d_scalar.p, sizeof(double) * (pair ? 2 : 1), cudaMemcpyDeviceToHost,
+                        c->stream));
+  RL_CK(cudaStreamSynchronize(c->stream));
+  *o0 = r[0];
+  if (pair) *o1 = r[1];
+  return RL_OK;
+}
+
+int rl_cddt_cast(rl_cddt* c, double x, double y, double theta, double* out) {
+  if (!c || !out) return RL_EINVAL;
+  return single(c, x, y, theta, 0, out, nullptr);
+}
+
+int rl_cddt_cast_pair(rl_cddt* c, double x, double y, double theta, double* f, double* b) {
+  if (!c || !f || !b) return RL_EINVAL;
+  return single(c, x, y, theta, 1, f, b);
+}
+
+int rl_cddt_cast_batch(rl_cddt* c, const float* x, const float* y, const float* theta, float* out,
+                       int32_t* hit, size_t n, void* stream) {
+  if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  k_cast<float><<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, theta, out,
+                                                                     hit, nullptr, nullptr, n);
+  return finish(c, stream);
+}
+
+int rl_cddt_cast_batch_f64(rl_cddt* c, const double* x, const double* y, const double* theta,
+                           double* out, int32_t* hit, int64_t* res_row, int32_t* res_idx,
+                           size_t n, void* stream) {
+  if (!c || (n && (!x || !y || !theta))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  k_cast<double><<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(
+      c->view(), x, y, theta, out, hit, res_row, res_idx, n);
+  return finish(c, stream);
+}
+
+int rl_cddt_directional_batch(rl_cddt* c, const double* x, const double* y, const int32_t* a,
+                              double* out, size_t n, void* stream) {
+  if (!c || (n && (!x || !y || !a || !out))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  k_directional<<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, a, out, n);
+  return finish(c, stream);
+}
+
+// Host-buffer batches: chunked H2D -> kernel -> D2H over NSTREAM streams so
+// both copy directions overlap the kernel.
+int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const float* theta,
+                            float* out, size_t n) {
+  if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  constexpr int NSTREAM = 3;
+  const size_t chunk = std::min<size_t>(n, size_t(1) << 22);  // 4M queries = 64 MB per chunk
+  struct Lane {
+    cudaStream_t s = nullptr;
+    DevBuf<float> buf;  // x | y | theta | out
+  };
+  static thread_local std::vector<Lane> lanes;  // reused across calls on this thread
+  static thread_local size_t lane_chunk = 0;
+  static thread_local int lane_dev = -1;
+  if (lanes.empty() || lane_chunk < chunk || lane_dev != c->dev) {
+    for (auto& l : lanes)
+      if (l.s) cudaStreamDestroy(l.s);
+    lanes.clear();
+    lanes.resize(NSTREAM);
+    for (auto& l : lanes) {
+      RL_CK(cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking));
+      RL_TRY(l.buf.alloc(4 * chunk));
+    }
+    lane_chunk = chunk;
+    lane_dev = c->dev;
+  }
+  cudaEvent_t ready;
+  RL_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
+  const size_t stride = lane_chunk;
+  size_t k = 0;
+  for (size_t off = 0; off < n; off += chunk, k++) {
+    Lane& l = lanes[k % NSTREAM];
+    const size_t m = std::min(chunk, n - off);
+    float* dx = l.buf.p;
+    float* dy = dx + stride;
+    float* dt = dy + stride;
+    float* dout = dt + stride;
+    RL_CK(cudaStreamWaitEvent(l.s, ready, 0));
+    RL_CK(cudaMemcpyAsync(dx, x + off, m * 4, cudaMemcpyHostToDevice, l.s));
+    RL_CK(cudaMemcpyAsync(dy, y + off, m * 4, cudaMemcpyHostToDevice, l.s));
+    RL_CK(cudaMemcpyAsync(dt, theta + off, m * 4, cudaMemcpyHostToDevice, l.s));
+    k_cast<float><<<cast_blocks(m), 256, 0, l.s>>>(c->view(), dx, dy, dt, dout, nullptr, nullptr,
+                                                    nullptr, m);
+    RL_CK(cudaGetLastError());
+    RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
+  }
+  for (auto& l : lanes) RL_CK(cudaStreamSynchronize(l.s));
+  cudaEventDestroy(ready);
+  return RL_OK;
+}
+
+int rl_cddt_export(const rl_cddt* c, uint32_t* slice_row_base, uint64_t* row_off, float* zp,
+                   uint8_t* membership, uint8_t* grid) {
+  if (!c) return RL_EINVAL;
+  DeviceGuard guard(c->dev);
+  RL_CK(cudaStreamSynchronize(c->stream));
+  if (slice_row_base) {
+    for (int s = 0; s < c->S; s++) slice_row_base[s] = c->slices[s].row_base;
+    slice_row_base[c->S] = uint32_t(c->rows);
+  }
+  if (row_off) {
+    std::vector<uint32_t> o(c->rows + 1);
+    RL_CK(cudaMemcpy(o.data(), c->row_off.p, sizeof(uint32_t) * (c->rows + 1),
+                     cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i <= c->rows; i++) row_off[i] = o[i];
+  }
+  if (zp && c->zero_points)
+    RL_CK(cudaMemcpy(zp, c->zp.p, sizeof(float) * c->zero_points, cudaMemcpyDeviceToHost));
+  const size_t wh = size_t(c->w) * c->h;
+  if (membership) std::memcpy(membership, c->member_h.data(), wh);
+  if (grid) std::memcpy(grid, c->grid_h.data(), wh);
+  return RL_OK;
+}
+
+}  // extern "C"

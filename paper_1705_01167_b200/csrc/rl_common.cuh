@@ -1,0 +1,143 @@
+// Host-side plumbing shared by the CUDA translation units: error state,
+// CUDA checks, device buffers, and the handle layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/rl_cddt.h"
+#include "cddt_device.cuh"
+
+namespace rl {
+
+void set_error(const char* fmt, ...);
+
+// Exception-free CUDA check: records the message and returns RL_ECUDA.
+#define RL_CK(call)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess) {                                                                 \
+      ::rl::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));    \
+      return e_ == cudaErrorMemoryAllocation ? RL_ENOMEM : RL_ECUDA;                         \
+    }                                                                                        \
+  } while (0)
+
+#define RL_TRY(expr)          \
+  do {                        \
+    int st_ = (expr);         \
+    if (st_ != RL_OK) return st_; \
+  } while (0)
+
+// Owning device allocation (cudaMalloc / cudaFree on the current device).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  int alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      set_error("cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+      return RL_ENOMEM;
+    }
+    n = count;
+    return RL_OK;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// Makes `dev` current for the lifetime of the guard.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace rl
+
+// The opaque handle (include/rl_cddt.h). Owns the device copy of the flags
+// and the CSR structure on one device, plus host mirrors of the grid and
+// membership (small: w*h bytes) that drive incremental edits.
+struct rl_cddt {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int w = 0, h = 0, K = 0, S = 0;
+  double max_range = 0.0, resolution = 0.05;
+  bool pruned = false;
+  double init_seconds = 0.0;
+
+  std::vector<double> dcos, dsin;      // K, host glibc (cddt.cpp:30-42)
+  std::vector<rl::SliceParam> slices;  // S
+  uint64_t rows = 0, zero_points = 0;
+
+  std::vector<uint8_t> grid_h;    // host mirror: occupancy
+  std::vector<uint8_t> member_h;  // host mirror: membership
+
+  rl::DevBuf<uint8_t> flags;        // w*h
+  rl::DevBuf<uint32_t> row_off;     // rows+1
+  rl::DevBuf<float> zp;             // capacity >= zero_points
+  rl::DevBuf<rl::SliceParam> d_slices;
+  rl::DevBuf<double2> d_dirs;
+  rl::DevBuf<double> d_scalar;      // scratch for single-query calls
+  rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
+
+  rl::CddtView view() const {
+    rl::CddtView v;
+    v.flags = flags.p;
+    v.row_off = row_off.p;
+    v.zp = zp.p;
+    v.slices = d_slices.p;
+    v.dirs = d_dirs.p;
+    v.w = w;
+    v.h = h;
+    v.K = K;
+    v.S = S;
+    v.max_range = max_range;
+    return v;
+  }
+};
+
+namespace rl {
+int sm_count();
+inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
+  return s ? static_cast<cudaStream_t>(s) : c->stream;
+}
+int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
+}  // namespace rl

@@ -1,0 +1,218 @@
+// Fused beam sensor model: sensor_update (proj/src/mcl.cpp:58-120) on the GPU.
+//
+// One CTA scores PB particles x nbeams beams: every (particle, beam) item is a
+// CDDT cast (cddt_device.cuh) followed by the likelihood lookup, the per-beam
+// log-likelihoods land in shared memory and one thread per particle sums them
+// in beam order 0..nbeams-1 — the reference's summation order, so the FP64
+// log-weight is reproducible. Normalisation (max-subtract, exp, sum, divide,
+// degenerate reset, mcl.cpp:108-119) follows as a reduction.
+#include <cub/cub.cuh>
+
+#include <cmath>
+
+#include "rl_common.cuh"
+
+namespace rl {
+
+constexpr int kSensorParticlesPerCta = 16;
+
+struct BeamParams {
+  double w_hit, w_short, w_max, w_rand, sigma_hit, lambda_short, z_max;
+};
+
+// beam_likelihood (mcl.cpp:11-40)
+__device__ __forceinline__ double beam_likelihood(const BeamParams& p, double expected,
+                                                  double measured) {
+  const double zm = p.z_max;
+  const double e = expected < 0.0 ? 0.0 : (zm < expected ? zm : expected);
+  const double m = measured < 0.0 ? 0.0 : (zm < measured ? zm : measured);
+  double hit = 0.0;
+  if (p.w_hit > 0.0) {
+    const double s = p.sigma_hit;
+    const double inv_sqrt2 = 0.7071067811865476;
+    double eta = 0.5 * (erf((zm - e) / s * inv_sqrt2) - erf((0.0 - e) / s * inv_sqrt2));
+    if (eta > 1e-12) {
+      double z = (m - e) / s;
+      hit = exp(-0.5 * z * z) / (s * 2.5066282746310002) / eta;
+    }
+  }
+  double shrt = 0.0;
+  if (p.w_short > 0.0 && e > 0.0 && m <= e) {
+    double denom = 1.0 - exp(-p.lambda_short * e);
+    if (denom > 1e-12) shrt = p.lambda_short * exp(-p.lambda_short * m) / denom;
+  }
+  double mx = (m >= zm - 1.0) ? 1.0 : 0.0;
+  double rnd = 1.0 / zm;
+  return p.w_hit * hit + p.w_short * shrt + p.w_max * mx + p.w_rand * rnd;
+}
+
+__device__ __forceinline__ int table_index(double r, double inv_res, int zdim) {
+  long i = iround(r * inv_res);
+  if (i < 0) i = 0;
+  if (i > zdim - 1) i = zdim - 1;
+  return int(i);
+}
+
+__global__ void __launch_bounds__(256) k_sensor_logw(
+    CddtView c, const double* __restrict__ px, const double* __restrict__ py,
+    const double* __restrict__ pt, size_t n, const double* __restrict__ scan, int nb, double fov,
+    BeamParams bp, const float* __restrict__ table, int zdim, double inv_res,
+    double* __restrict__ logw) {
+  extern __shared__ double ll[];  // [PB][nb]
+  const size_t p0 = size_t(blockIdx.x) * kSensorParticlesPerCta;
+  const int items = kSensorParticlesPerCta * nb;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int pl = it / nb, b = it % nb;
+    const size_t i = p0 + pl;
+    if (i >= n) continue;
+    // ScanSpec::beam_offset (mcl.hpp:42-51)
+    const double off = nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);
+    const double th = normalize_angle_2pi(pt[i] + off);
+    CastOut o;
+    const double e = directional_cast(c, px[i], py[i], direction_index(th, c.K), o);
+    const double m = scan[b];
+    double like;
+    if (table)
+      like = double(__ldg(table + size_t(table_index(m, inv_res, zdim)) * zdim +
+                          table_index(e, inv_res, zdim)));
+    else
+      like = beam_likelihood(bp, e, m);
+    ll[it] = log(like);
+  }
+  __syncthreads();
+  if (threadIdx.x < kSensorParticlesPerCta) {
+    const size_t i = p0 + threadIdx.x;
+    if (i < n) {
+      double lw = 0.0;
+      const double* row = ll + threadIdx.x * nb;
+      for (int b = 0; b < nb; b++) lw += row[b];  // mcl.cpp:102-103 order
+      logw[i] = lw;
+    }
+  }
+}
+
+__global__ void k_exp_shift(const double* __restrict__ logw, const double* __restrict__ mx,
+                            double* __restrict__ w, size_t n) {
+  const double m = *mx;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    w[i] = exp(logw[i] - m);
+}
+
+__global__ void k_normalise(double* __restrict__ w, const double* __restrict__ sum, size_t n,
+                            int* __restrict__ degenerate) {
+  const double s = *sum;
+  const bool bad = !(s > 0.0) || !isfinite(s);  // mcl.cpp:114
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    w[i] = bad ? 1.0 / double(n) : w[i] / s;
+  if (bad && blockIdx.x == 0 && threadIdx.x == 0) *degenerate = 1;
+}
+
+static int blocks_for(size_t work, int threads) {
+  size_t b = (work + threads - 1) / threads;
+  size_t cap = size_t(sm_count()) * 16;
+  return int(std::max<size_t>(1, std::min(b, cap)));
+}
+
+}  // namespace rl
+
+using namespace rl;
+
+extern "C" {
+
+double rl_beam_likelihood(const rl_beam_params_t* p, double expected, double measured) {
+  // host restatement of beam_likelihood (mcl.cpp:11-40) for table building
+  const double zm = p->z_max;
+  if (!(zm > 0.0)) return NAN;
+  const double e = expected < 0.0 ? 0.0 : (zm < expected ? zm : expected);
+  const double m = measured < 0.0 ? 0.0 : (zm < measured ? zm : measured);
+  double hit = 0.0;
+  if (p->w_hit > 0.0) {
+    const double s = p->sigma_hit;
+    const double inv_sqrt2 = 0.7071067811865476;
+    double eta =
+        0.5 * (std::erf((zm - e) / s * inv_sqrt2) - std::erf((0.0 - e) / s * inv_sqrt2));
+    if (eta > 1e-12) {
+      double z = (m - e) / s;
+      hit = std::exp(-0.5 * z * z) / (s * 2.5066282746310002) / eta;
+    }
+  }
+  double shrt = 0.0;
+  if (p->w_short > 0.0 && e > 0.0 && m <= e) {
+    double denom = 1.0 - std::exp(-p->lambda_short * e);
+    if (denom > 1e-12) shrt = p->lambda_short * std::exp(-p->lambda_short * m) / denom;
+  }
+  double mx = (m >= zm - 1.0) ? 1.0 : 0.0;
+  double rnd = 1.0 / zm;
+  return p->w_hit * hit + p->w_short * shrt + p->w_max * mx + p->w_rand * rnd;
+}
+
+int rl_beam_table(const rl_beam_params_t* p, int32_t zdim, double inv_res, float* table) {
+  if (!p || !table || zdim <= 0 || !(inv_res > 0.0)) return RL_EINVAL;
+  if (!(p->z_max > 0.0)) {
+    set_error("beam model z_max must be positive");  // mcl.cpp:13
+    return RL_EINVAL;
+  }
+  for (int m = 0; m < zdim; m++)
+    for (int e = 0; e < zdim; e++)
+      table[size_t(m) * zdim + e] =
+          float(rl_beam_likelihood(p, double(e) / inv_res, double(m) / inv_res));
+  return RL_OK;
+}
+
+int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const double* pt, size_t n,
+                     const double* scan, int32_t nbeams, double fov,
+                     const rl_beam_params_t* params, const float* table, int32_t zdim,
+                     double inv_res, double* logw, double* weight, void* stream) {
+  if (!c || nbeams <= 0 || (n && (!px || !py || !pt || !scan))) {
+    set_error("scan length does not match beam count");  // mcl.cpp:61-62
+    return RL_EINVAL;
+  }
+  if (!table && (!params || !(params->z_max > 0.0))) {
+    set_error("beam model z_max must be positive");
+    return RL_EINVAL;
+  }
+  if (table && (zdim <= 0 || !(inv_res > 0.0))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  cudaStream_t st = pick_stream(c, stream);
+  // workspace: logw (if not given) | w (if not given) | max | sum | flag | cub temp
+  size_t cub_bytes = 0, cub2 = 0;
+  cub::DeviceReduce::Max(nullptr, cub_bytes, (double*)nullptr, (double*)nullptr, int(n), st);
+  cub::DeviceReduce::Sum(nullptr, cub2, (double*)nullptr, (double*)nullptr, int(n), st);
+  cub_bytes = std::max(cub_bytes, cub2);
+  const size_t need = 16 * n + 64 + cub_bytes + 256;
+  if (c->ws.n < need) RL_TRY(c->ws.alloc(need));
+  uint8_t* base = c->ws.p;
+  double* d_logw = logw ? logw : reinterpret_cast<double*>(base);
+  double* d_w = weight ? weight : reinterpret_cast<double*>(base + 8 * n);
+  double* d_max = reinterpret_cast<double*>(base + 16 * n);
+  double* d_sum = d_max + 1;
+  int* d_flag = reinterpret_cast<int*>(d_max + 2);
+  void* d_tmp = base + 16 * n + 64;
+  BeamParams bp{};
+  if (params)
+    bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
+                    params->sigma_hit, params->lambda_short, params->z_max};
+  const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
+  const size_t smem = sizeof(double) * kSensorParticlesPerCta * nbeams;
+  if (smem > 48 * 1024)
+    RL_CK(cudaFuncSetAttribute(k_sensor_logw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  k_sensor_logw<<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nbeams, fov, bp, table,
+                                         zdim, inv_res, d_logw);
+  RL_CK(cudaGetLastError());
+  RL_CK(cub::DeviceReduce::Max(d_tmp, cub_bytes, d_logw, d_max, int(n), st));
+  k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(d_logw, d_max, d_w, n);
+  RL_CK(cub::DeviceReduce::Sum(d_tmp, cub_bytes, d_w, d_sum, int(n), st));
+  RL_CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+  k_normalise<<<blocks_for(n, 256), 256, 0, st>>>(d_w, d_sum, n, d_flag);
+  RL_CK(cudaGetLastError());
+  int flag = 0;
+  RL_CK(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+  return flag ? RL_EDEGENERATE : RL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,342 @@
+// Incremental map updates: Cddt::set_occupancy (proj/src/cddt.cpp:332-377)
+// applied to a batch of edits.
+//
+// The reference maintains the invariant that after any edit sequence the bins
+// equal a fresh build of the final grid (proj/tests/test_cddt.cpp:578-604):
+// membership is exactly the edge map, and each member pixel contributes
+// float(project_x(centre)) to every row its square overlaps. A batch is
+// therefore applied as a set difference against the current structure:
+//   1. host: replay the edits in order on the host grid mirror (last writer
+//      wins), collect cells whose occupancy changed;
+//   2. host: recompute occupancy/clear/membership flags in the 1-cell dilation
+//      of those cells; cells whose membership flipped are the delta pixels;
+//   3. device: expand delta pixels to (row, value, +/-1) records over all
+//      slices, radix-sort them by (row, value);
+//   4. device: new row lengths -> scan -> per-row merge of the old sorted row
+//      with its sorted deltas (unaffected rows are a straight copy).
+// Only O(changed pixels * S) records are sorted; the copy is one pass over
+// the zero-point array.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <unordered_map>
+
+#include "rl_common.cuh"
+
+namespace rl {
+
+// same as in rl_cddt.cu (kept local: device code is per-TU)
+__device__ __forceinline__ void pixel_rows_u(const SliceParam& sp, int px, int py, int& r0,
+                                             int& r1, float& v) {
+  auto py_of = [&](double x, double y) { return -x * sp.sin_t + y * sp.cos_t + sp.y_offset; };
+  double c0 = py_of(double(px), double(py));
+  double c1 = py_of(double(px + 1), double(py));
+  double c2 = py_of(double(px), double(py + 1));
+  double c3 = py_of(double(px + 1), double(py + 1));
+  double lo = fmin_std(fmin_std(c0, c1), fmin_std(c2, c3));
+  double hi = fmax_std(fmax_std(c0, c1), fmax_std(c2, c3));
+  r0 = int(floor(lo));
+  r1 = int(ceil(hi)) - 1;
+  if (r0 < 0) r0 = 0;
+  if (r1 >= sp.bin_count) r1 = sp.bin_count - 1;
+  const double cx = double(px) + 0.5, cy = double(py) + 0.5;
+  v = __double2float_rn(cx * sp.cos_t + cy * sp.sin_t);
+}
+
+// order-preserving map f32 -> u32 (negatives flipped)
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// delta pixel (cell, sign) x slice -> records key = row<<32 | f2key(v), val = sign
+__global__ void k_delta_records(const int32_t* __restrict__ cells, const int8_t* __restrict__ sign,
+                                int n_cells, const SliceParam* __restrict__ slices, int S, int w,
+                                unsigned long long* __restrict__ keys, int8_t* __restrict__ vals,
+                                unsigned* __restrict__ count, int32_t* __restrict__ add_cnt,
+                                int32_t* __restrict__ rem_cnt) {
+  const int total = n_cells * S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int k = i / S, s = i % S;
+    const int cell = cells[k];
+    const SliceParam sp = slices[s];
+    int r0, r1;
+    float v;
+    pixel_rows_u(sp, cell % w, cell / w, r0, r1, v);
+    for (int r = r0; r <= r1; r++) {
+      const uint32_t g = sp.row_base + uint32_t(r);
+      unsigned pos = atomicAdd(count, 1u);
+      keys[pos] = (static_cast<unsigned long long>(g) << 32) | f2key(v);
+      vals[pos] = sign[k];
+      if (sign[k] > 0)
+        atomicAdd(&add_cnt[g], 1);
+      else
+        atomicAdd(&rem_cnt[g], 1);
+    }
+  }
+}
+
+__global__ void k_new_len(const uint32_t* __restrict__ off, const int32_t* __restrict__ add_cnt,
+                          const int32_t* __restrict__ rem_cnt, uint32_t* __restrict__ len,
+                          size_t rows) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
+       g += size_t(gridDim.x) * blockDim.x)
+    len[g] = g < rows ? (off[g + 1] - off[g]) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]) : 0u;
+}
+
+// One warp per row. Unaffected rows: coalesced copy. Affected rows: lane 0
+// merges the old row with the row's sorted deltas (ZeroPointBin::insert /
+// remove_one semantics, cddt.hpp:67-84: removing takes out one element equal
+// to the value; equal keys are bit-identical so their order is immaterial).
+__global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* __restrict__ old_zp,
+                             const uint32_t* __restrict__ new_off, float* __restrict__ new_zp,
+                             const int32_t* __restrict__ add_cnt,
+                             const int32_t* __restrict__ rem_cnt,
+                             const unsigned long long* __restrict__ keys,
+                             const int8_t* __restrict__ vals, unsigned n_rec, size_t rows,
+                             unsigned* __restrict__ unmatched) {
+  const unsigned lane = threadIdx.x & 31;
+  const size_t warp = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
+  const size_t nwarps = (size_t(gridDim.x) * blockDim.x) >> 5;
+  for (size_t g = warp; g < rows; g += nwarps) {
+    const uint32_t a = old_off[g], b = old_off[g + 1];
+    const uint32_t o = new_off[g];
+    if (add_cnt[g] == 0 && rem_cnt[g] == 0) {
+      for (uint32_t i = a + lane; i < b; i += 32) new_zp[o + (i - a)] = old_zp[i];
+      continue;
+    }
+    if (lane != 0) continue;
+    // delta range of row g: lower_bound of g<<32 in the sorted keys
+    const unsigned long long lo_key = static_cast<unsigned long long>(g) << 32;
+    unsigned lo = 0, len = n_rec;
+    while (len > 0) {
+      unsigned half = len >> 1, mid = lo + half;
+      if (keys[mid] < lo_key) {
+        lo = mid + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    unsigned j = lo;
+    const unsigned jend = lo + unsigned(add_cnt[g] + rem_cnt[g]);
+    uint32_t i = a, w = o;
+    unsigned miss = 0;
+    while (i < b || j < jend) {
+      if (j < jend) {
+        const float dv = __uint_as_float((keys[j] & 0x80000000ull) ? uint32_t(keys[j]) & 0x7fffffffu
+                                                                    : ~uint32_t(keys[j]));
+        if (i == b || dv < old_zp[i]) {
+          if (vals[j] > 0)
+            new_zp[w++] = dv;
+          else
+            miss++;
+          j++;
+          continue;
+        }
+        if (dv == old_zp[i]) {
+          if (vals[j] > 0) {
+            new_zp[w++] = dv;
+          } else {
+            i++;  // remove_one: drop one equal element
+          }
+          j++;
+          continue;
+        }
+      }
+      new_zp[w++] = old_zp[i++];
+    }
+    if (miss) atomicAdd(unmatched, miss);
+  }
+}
+
+__global__ void k_set_flags(const int32_t* __restrict__ cells, const uint8_t* __restrict__ f,
+                            int n, uint8_t* __restrict__ flags) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    flags[cells[i]] = f[i];
+}
+
+static int blocks_for(size_t work, int threads, int cap_per_sm = 16) {
+  size_t b = (work + threads - 1) / threads;
+  size_t cap = size_t(sm_count()) * cap_per_sm;
+  return int(std::max<size_t>(1, std::min(b, cap)));
+}
+
+// Apply edits [0, n) (already validated) to the structure.
+static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n) {
+  const int w = c->w, h = c->h;
+  auto at = [&](int x, int y) { return c->grid_h[size_t(y) * w + x] != 0; };
+  auto inb = [&](int x, int y) { return x >= 0 && y >= 0 && x < w && y < h; };
+  // 1. replay in order; remember each touched cell's original state
+  std::unordered_map<int32_t, uint8_t> orig;
+  orig.reserve(n * 2);
+  for (size_t k = 0; k < n; k++) {
+    const int32_t cell = xy[2 * k + 1] * w + xy[2 * k];
+    orig.emplace(cell, c->grid_h[cell]);
+    c->grid_h[cell] = occ[k] ? 1 : 0;
+  }
+  std::vector<int32_t> changed;
+  for (auto& kv : orig)
+    if (kv.second != c->grid_h[kv.first]) changed.push_back(kv.first);
+  if (changed.empty()) return RL_OK;
+  // 2. flags in the dilation; membership deltas
+  std::unordered_map<int32_t, uint8_t> window;
+  for (int32_t cell : changed) {
+    const int x = cell % w, y = cell / w;
+    for (int dy = -1; dy <= 1; dy++)
+      for (int dx = -1; dx <= 1; dx++)
+        if (inb(x + dx, y + dy)) window.emplace((y + dy) * w + (x + dx), 0);
+  }
+  std::vector<int32_t> wcells, dcells;
+  std::vector<uint8_t> wflags;
+  std::vector<int8_t> dsign;
+  wcells.reserve(window.size());
+  for (auto& kv : window) {
+    const int32_t cell = kv.first;
+    const int x = cell % w, y = cell / w;
+    const bool o = at(x, y);
+    bool any_occ = false, any_free = false;
+    for (int dy = -1; dy <= 1; dy++)
+      for (int dx = -1; dx <= 1; dx++) {
+        if (dx == 0 && dy == 0) continue;
+        const int nx = x + dx, ny = y + dy;
+        if (!inb(nx, ny) || !at(nx, ny))
+          any_free = true;
+        else
+          any_occ = true;
+      }
+    const bool member = o && any_free;  // is_edge_cell (grid.cpp:110-119)
+    uint8_t f = 0;
+    if (o) f |= kOcc;
+    if (!o && !any_occ) f |= kClear;  // clear_around (cddt.cpp:173-180)
+    if (member) f |= kMember;
+    wcells.push_back(cell);
+    wflags.push_back(f);
+    if (member != (c->member_h[cell] != 0)) {
+      dcells.push_back(cell);
+      dsign.push_back(member ? 1 : -1);
+      c->member_h[cell] = member ? 1 : 0;
+    }
+  }
+  cudaStream_t st = c->stream;
+  DevBuf<int32_t> d_wcells;
+  DevBuf<uint8_t> d_wflags;
+  RL_TRY(d_wcells.alloc(wcells.size()));
+  RL_TRY(d_wflags.alloc(wflags.size()));
+  RL_CK(cudaMemcpyAsync(d_wcells.p, wcells.data(), 4 * wcells.size(), cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemcpyAsync(d_wflags.p, wflags.data(), wflags.size(), cudaMemcpyHostToDevice, st));
+  k_set_flags<<<blocks_for(wcells.size(), 256), 256, 0, st>>>(d_wcells.p, d_wflags.p,
+                                                              int(wcells.size()), c->flags.p);
+  RL_CK(cudaGetLastError());
+  if (dcells.empty()) return RL_OK;
+
+  // 3. delta records
+  const int nd = int(dcells.size());
+  const size_t cap = size_t(nd) * c->S * 3;  // a unit square spans at most 3 rows
+  DevBuf<int32_t> d_dcells, add_cnt, rem_cnt;
+  DevBuf<int8_t> d_dsign, vals, vals_sorted;
+  DevBuf<unsigned long long> keys, keys_sorted;
+  DevBuf<unsigned> d_count;
+  RL_TRY(d_dcells.alloc(nd));
+  RL_TRY(d_dsign.alloc(nd));
+  RL_TRY(add_cnt.alloc(c->rows));
+  RL_TRY(rem_cnt.alloc(c->rows));
+  RL_TRY(keys.alloc(cap));
+  RL_TRY(vals.alloc(cap));
+  RL_TRY(keys_sorted.alloc(cap));
+  RL_TRY(vals_sorted.alloc(cap));
+  RL_TRY(d_count.alloc(2));
+  RL_CK(cudaMemcpyAsync(d_dcells.p, dcells.data(), 4 * nd, cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemcpyAsync(d_dsign.p, dsign.data(), nd, cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemsetAsync(add_cnt.p, 0, 4 * c->rows, st));
+  RL_CK(cudaMemsetAsync(rem_cnt.p, 0, 4 * c->rows, st));
+  RL_CK(cudaMemsetAsync(d_count.p, 0, 8, st));
+  k_delta_records<<<blocks_for(size_t(nd) * c->S, 256), 256, 0, st>>>(
+      d_dcells.p, d_dsign.p, nd, c->d_slices.p, c->S, w, keys.p, vals.p, d_count.p, add_cnt.p,
+      rem_cnt.p);
+  RL_CK(cudaGetLastError());
+  unsigned n_rec = 0;
+  RL_CK(cudaMemcpyAsync(&n_rec, d_count.p, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, vals.p,
+                                    vals_sorted.p, int(n_rec), 0, 64, st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_sorted.p, vals.p,
+                                          vals_sorted.p, int(n_rec), 0, 64, st));
+  }
+  // 4. new offsets and merge
+  DevBuf<uint32_t> len, new_off;
+  RL_TRY(len.alloc(c->rows + 1));
+  RL_TRY(new_off.alloc(c->rows + 1));
+  k_new_len<<<blocks_for(c->rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt.p, rem_cnt.p,
+                                                          len.p, c->rows);
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len.p, new_off.p, int(c->rows + 1), st);
+    DevBuf<uint8_t> tmp;
+    RL_TRY(tmp.alloc(tmp_bytes));
+    RL_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, len.p, new_off.p, int(c->rows + 1), st));
+  }
+  uint32_t total = 0;
+  RL_CK(cudaMemcpyAsync(&total, new_off.p + c->rows, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+  DevBuf<float> nzp;
+  RL_TRY(nzp.alloc(total));
+  k_merge_rows<<<blocks_for(c->rows * 32, 256, 32), 256, 0, st>>>(
+      c->row_off.p, c->zp.p, new_off.p, nzp.p, add_cnt.p, rem_cnt.p, keys_sorted.p, vals_sorted.p,
+      n_rec, c->rows, d_count.p + 1);
+  RL_CK(cudaGetLastError());
+  unsigned miss = 0;
+  RL_CK(cudaMemcpyAsync(&miss, d_count.p + 1, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+  if (miss) {
+    set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)", miss);
+    return RL_ELOGIC;
+  }
+  c->zp = std::move(nzp);
+  c->row_off = std::move(new_off);
+  c->zero_points = total;
+  return RL_OK;
+}
+
+}  // namespace rl
+
+using namespace rl;
+
+extern "C" {
+
+int rl_cddt_set_occupancy_batch(rl_cddt* c, const int32_t* xy, const uint8_t* occupied,
+                                size_t n) {
+  if (!c || (n && (!xy || !occupied))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  if (c->pruned) {
+    set_error("cddt: incremental updates are disabled after prune");  // cddt.cpp:333
+    return RL_ELOGIC;
+  }
+  size_t valid = n;
+  for (size_t k = 0; k < n; k++) {
+    const int x = xy[2 * k], y = xy[2 * k + 1];
+    if (x < 0 || y < 0 || x >= c->w || y >= c->h) {
+      valid = k;
+      break;
+    }
+  }
+  DeviceGuard guard(c->dev);
+  RL_TRY(apply_edits(c, xy, occupied, valid));
+  if (valid < n) {
+    set_error("cddt: cell outside the grid");  // cddt.cpp:334
+    return RL_ERANGE;
+  }
+  return RL_OK;
+}
+
+int rl_cddt_set_occupancy(rl_cddt* c, int32_t x, int32_t y, int32_t occupied) {
+  int32_t xy[2] = {x, y};
+  uint8_t o = occupied ? 1 : 0;
+  return rl_cddt_set_occupancy_batch(c, xy, &o, 1);
+}
+
+}  // extern "C"

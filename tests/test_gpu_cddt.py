@@ -1,0 +1,347 @@
+"""GPU parity: construction, queries, pruning, edits and snapshots of the CUDA
+CDDT against the unmodified reference (oracle/_ref) and the C restatement
+(oracle/), on the same seeded inputs. Bit-exact everywhere: zero-point arrays,
+row offsets, membership, FP64 ranges, hit cells and resolving indices."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def fig4():
+    # proj/tests/support/oracles.hpp:19-26
+    g = np.zeros((4, 4), np.uint8)
+    g[0, 3] = g[1, 1] = g[2, 2] = g[3, 3] = 1
+    return g
+
+
+def random_map(w, h, density, seed):
+    # make_random_map (proj/src/synthetic.cpp:84-93): SplitMix64 uniform < density
+    s = np.uint64(seed)
+    out = np.zeros(w * h, np.uint8)
+    m64 = (1 << 64) - 1
+    st = seed & m64
+    for i in range(w * h):
+        st = (st + 0x9E3779B97F4A7C15) & m64
+        z = st
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m64
+        z ^= z >> 31
+        out[i] = 1 if (z >> 11) * 2.0 ** -53 < density else 0
+    del s
+    return out.reshape(h, w)
+
+
+def make_gpu(rl, g, K, max_range=0.0, prune=False):
+    grid = rl.OccupancyGrid.from_array(g)
+    return rl.Cddt(grid, rl.RangeMethodConfig(max_range, K), prune=prune)
+
+
+def assert_same_structure(gpu, ref_export):
+    e = gpu.export()
+    assert np.array_equal(e["row_off"], ref_export["row_off"])
+    assert np.array_equal(e["zp"].view(np.uint32), ref_export["zp"].view(np.uint32))
+    assert np.array_equal(e["membership"], ref_export["membership"])
+
+
+def test_fig4_bins_and_fixtures(rl):
+    # proj/tests/test_cddt.cpp:229-242 and :349-360
+    c = make_gpu(rl, fig4(), 8)
+    assert c.theta_disc() == 8 and c.slice_count() == 4
+    assert c.max_range() == pytest.approx(math.sqrt(32.0))
+    assert c.slice(0).bin_count == 5
+    assert c.bin(0, 0).values() == [3.5]
+    assert c.bin(0, 1).values() == [1.5]
+    assert c.bin(0, 2).values() == [2.5]
+    assert c.bin(0, 3).values() == [3.5]
+    assert c.bin(0, 4).empty()
+    mr = c.max_range()
+    Q = rl.RayQuery
+    assert c.cast(Q(0.5, 0.5, 0.0)) == pytest.approx(3.0)
+    assert c.cast(Q(2.5, 1.5, 0.0)) == pytest.approx(mr)
+    assert c.cast(Q(2.5, 0.5, rl.kTwoPi / 2.0)) == pytest.approx(mr)
+    assert c.cast(Q(3.7, 1.5, rl.kTwoPi / 2.0)) == pytest.approx(2.2)
+    assert c.cast(Q(3.7, 2.5, rl.kTwoPi / 2.0)) == pytest.approx(0.7)
+    assert c.cast(Q(1.5, 1.5, 0.3)) == pytest.approx(0.0)
+    assert c.cast(Q(-0.5, 1.5, 0.0)) == pytest.approx(mr)
+    assert c.cast(Q(0.5, 4.5, 0.0)) == pytest.approx(mr)
+
+
+def test_corridor_cast_pair(rl):
+    # proj/tests/test_cddt.cpp:445-462
+    g = np.zeros((1, 5), np.uint8)
+    g[0, 0] = g[0, 4] = 1
+    c = make_gpu(rl, g, 8)
+    f, b = c.cast_pair(rl.RayQuery(2.5, 0.5, 0.0))
+    assert f == pytest.approx(2.0) and b == pytest.approx(2.0)
+    g2 = np.zeros((1, 5), np.uint8)
+    g2[0, 4] = 1
+    c2 = make_gpu(rl, g2, 8)
+    f, b = c2.cast_pair(rl.RayQuery(1.5, 0.5, 0.0))
+    assert f == pytest.approx(3.0) and b == pytest.approx(c2.max_range())
+
+
+def test_config_validation_errors(rl):
+    grid = rl.OccupancyGrid.from_array(fig4())
+    with pytest.raises(ValueError):
+        rl.Cddt(grid, rl.RangeMethodConfig(0.0, 7))
+    with pytest.raises(ValueError):
+        rl.Cddt(grid, rl.RangeMethodConfig(-1.0, 8))
+
+
+def test_empty_grid(rl):
+    # proj/tests/test_cddt.cpp:244-250
+    c = make_gpu(rl, np.zeros((9, 12), np.uint8), 12)
+    assert c.zero_point_count() == 0
+    assert c.cast(rl.RayQuery(6.0, 4.5, 1.0)) == pytest.approx(c.max_range())
+
+
+@pytest.mark.parametrize("case", ["fig4", "rand64", "rand_ragged", "full", "cfg1", "line"])
+def test_build_bitexact_vs_reference(rl, oracle_mod, synth, case):
+    K, mr = 108, 0.0
+    if case == "fig4":
+        g, K = fig4(), 8
+    elif case == "rand64":
+        g, K = random_map(64, 64, 0.08, 1001), 216
+    elif case == "rand_ragged":
+        g, K = random_map(37, 5, 0.2, 7), 24
+    elif case == "full":
+        g, K = np.ones((16, 9), np.uint8), 12
+    elif case == "line":
+        g, K = np.zeros((20, 20), np.uint8), 16
+        g[7, 5:15] = 1
+    else:
+        g, K, mr = synth.rect_map(), 108, 300.0
+    gpu = make_gpu(rl, g, K, mr)
+    ref = (oracle_mod.RefCddt if oracle_mod.ref_available() else oracle_mod.OracleCddt)(g, K, mr)
+    assert gpu.info().rows == ref.info()["rows"]
+    assert gpu.zero_point_count() == ref.info()["zero_points"]
+    assert gpu.memory_bytes() == ref.info()["memory_bytes"]
+    assert_same_structure(gpu, ref.export())
+
+
+def test_casts_bitexact_cfg1(rl, oracle_mod, synth):
+    import torch
+    g = synth.rect_map()
+    gpu = make_gpu(rl, g, 108, 300.0)
+    qx, qy, qt = synth.free_queries(g, 100_000, seed=7)
+    orc = oracle_mod.OracleCddt(g, 108, 300.0).cast_batch(qx, qy, qt)
+    # f64 path with hit cell and resolving index
+    x, y, t = (dev(a.astype(np.float64)) for a in (qx, qy, qt))
+    n = qx.size
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    hit = torch.empty(n, dtype=torch.int32, device="cuda")
+    rr = torch.empty(n, dtype=torch.int64, device="cuda")
+    ri = torch.empty(n, dtype=torch.int32, device="cuda")
+    gpu.cast_batch_f64(x, y, t, out, hit, rr, ri)
+    torch.cuda.synchronize()
+    assert np.array_equal(host(out).view(np.uint64), orc["out64"].view(np.uint64))
+    assert np.array_equal(host(hit), orc["hit"])
+    assert np.array_equal(host(rr), orc["res_row"])
+    assert np.array_equal(host(ri), orc["res_idx"])
+    if oracle_mod.ref_available():
+        ref = oracle_mod.RefCddt(g, 108, 300.0).cast_batch(qx, qy, qt)
+        assert np.array_equal(host(out).view(np.uint64), ref["out64"].view(np.uint64))
+        assert np.array_equal(host(rr), ref["res_row"])
+        assert np.array_equal(host(ri), ref["res_idx"])
+    # f32 device path == float(reference f64)
+    o32 = gpu.cast_batch(dev(qx), dev(qy), dev(qt), hit=hit)
+    torch.cuda.synchronize()
+    assert np.array_equal(host(o32), orc["out64"].astype(np.float32))
+    assert np.array_equal(host(hit), orc["hit"])
+    # host pipelined path
+    oh = gpu.cast_batch(qx, qy, qt)
+    assert np.array_equal(oh, orc["out32"])
+
+
+def test_casts_edge_inputs(rl, oracle_mod):
+    """Off-map, on-lattice, exact-axis, huge/negative angles, zero-length batch."""
+    import torch
+    g = random_map(48, 40, 0.1, 99)
+    gpu = make_gpu(rl, g, 24, 0.0)
+    orc = oracle_mod.OracleCddt(g, 24, 0.0)
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.uniform(-2, 50, 2000), np.arange(0, 48, 0.5), [-0.0, 48.0, 47.999]])
+    ys = np.concatenate([rng.uniform(-2, 42, 2000), np.arange(0, 40, 40 / 96), [0.0, 39.99, 40.0]])
+    n = min(xs.size, ys.size)
+    xs, ys = xs[:n].astype(np.float32), ys[:n].astype(np.float32)
+    ts = np.concatenate([rng.uniform(-20, 20, n - 8),
+                         [0, np.pi / 2, np.pi, 3 * np.pi / 2, 2 * np.pi, -1e-7, 1e4, -1e4]])
+    ts = ts.astype(np.float32)
+    want = orc.cast_batch(xs, ys, ts)
+    got = gpu.cast_batch(dev(xs), dev(ys), dev(ts))
+    torch.cuda.synchronize()
+    assert np.array_equal(host(got), want["out32"])
+    empty = torch.empty(0, dtype=torch.float32, device="cuda")
+    gpu.cast_batch(empty, empty, empty)
+
+
+def test_cast_pair_equals_two_casts(rl, oracle_mod):
+    # proj/tests/test_cddt.cpp:430-443
+    g = random_map(32, 32, 0.1, 3)
+    gpu = make_gpu(rl, g, 24)
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        q = rl.RayQuery(rng.uniform(-1, 33), rng.uniform(-1, 33), rng.uniform(0, rl.kTwoPi))
+        f, b = gpu.cast_pair(q)
+        assert f == gpu.cast(q)
+        assert b == gpu.cast(rl.RayQuery(q.x, q.y, q.theta + rl.kTwoPi / 2.0))
+
+
+@pytest.mark.parametrize("case", ["rand20", "line", "block", "cfg1"])
+def test_prune_bitexact(rl, oracle_mod, synth, case):
+    K, mr = 16, 0.0
+    if case == "rand20":
+        g = random_map(20, 20, 0.1, 51)
+    elif case == "line":
+        g = np.zeros((20, 20), np.uint8)
+        g[7, 5:15] = 1
+    elif case == "block":
+        g, K = np.zeros((5, 5), np.uint8), 8
+        g[1:4, 1:4] = 1
+    else:
+        g, K, mr = synth.rect_map(), 108, 300.0
+    gpu = make_gpu(rl, g, K, mr, prune=True)
+    assert gpu.pruned()
+    ref = (oracle_mod.RefCddt if oracle_mod.ref_available() else oracle_mod.OracleCddt)(
+        g, K, mr, prune=True)
+    assert gpu.zero_point_count() == ref.info()["zero_points"]
+    assert_same_structure(gpu, ref.export())
+    if case == "line":
+        assert gpu.bin(0, 7).size() <= 2  # proj/tests/test_cddt.cpp:503-512
+    with pytest.raises(rl.LogicError):
+        gpu.set_occupancy(0, 0, True)
+
+
+def test_prune_preserves_discrete_states(rl, oracle_mod):
+    # proj/tests/test_cddt.cpp:464-484 on the GPU: PCDDT == CDDT at every
+    # (cell centre, direction) state
+    import torch
+    g = random_map(24, 24, 0.1, 53)
+    K = 16
+    full = make_gpu(rl, g, K)
+    pr = make_gpu(rl, g, K, prune=True)
+    ys, xs, aa = np.meshgrid(np.arange(24), np.arange(24), np.arange(K), indexing="ij")
+    x = dev(xs.ravel().astype(np.float64) + 0.5)
+    y = dev(ys.ravel().astype(np.float64) + 0.5)
+    a = dev(aa.ravel().astype(np.int32))
+    r0 = full.directional_batch(x, y, a)
+    r1 = pr.directional_batch(x, y, a)
+    torch.cuda.synchronize()
+    assert torch.equal(r0, r1)
+
+
+def test_set_occupancy_errors(rl):
+    c = make_gpu(rl, fig4(), 8)
+    with pytest.raises(IndexError):
+        c.set_occupancy(-1, 0, True)
+    with pytest.raises(IndexError):
+        c.set_occupancy(0, 4, True)
+    n = c.zero_point_count()
+    c.set_occupancy(1, 1, True)  # already occupied: no-op
+    c.set_occupancy(0, 0, False)
+    assert c.zero_point_count() == n
+
+
+def test_edits_match_reference_sequence(rl, oracle_mod):
+    # proj/tests/test_cddt.cpp:578-604: random edits, compared after each batch
+    g = random_map(16, 16, 0.1, 14)
+    K = 8
+    gpu = make_gpu(rl, g, K)
+    ref = (oracle_mod.RefCddt if oracle_mod.ref_available() else oracle_mod.OracleCddt)(g, K)
+    rng = np.random.default_rng(1000)
+    for rnd in range(6):
+        xy = rng.integers(0, 16, size=(10, 2)).astype(np.int32)
+        occ = rng.integers(0, 2, size=10).astype(np.uint8)
+        for (x, y), o in zip(xy, occ):
+            ref.set_occupancy(int(x), int(y), bool(o))
+        if rnd % 2:
+            gpu.set_occupancy_batch(xy, occ)
+        else:
+            for (x, y), o in zip(xy, occ):
+                gpu.set_occupancy(int(x), int(y), bool(o))
+        assert gpu.zero_point_count() == ref.info()["zero_points"]
+        assert_same_structure(gpu, ref.export())
+
+
+def test_block_edit_rounds_maze(rl, oracle_mod, synth):
+    """Config-5 style rounds (3x3 insert/remove blocks) on a 400x400 maze:
+    structure bit-exact with the sequential oracle after every round, and
+    equal to a fresh GPU build of the edited grid."""
+    g = synth.maze_map(400, 400, 0.10, 5)
+    K = 108
+    gpu = make_gpu(rl, g, K)
+    orc = oracle_mod.OracleCddt(g, K)
+    for rnd in range(5):
+        xy, occ = synth.block_edits(400, 400, 50, seed=100 + rnd)
+        for (x, y), o in zip(xy, occ):
+            orc.set_occupancy(int(x), int(y), bool(o))
+        gpu.set_occupancy_batch(xy, occ)
+        assert_same_structure(gpu, orc.export())
+    fresh = make_gpu(rl, gpu.export()["grid"], K)
+    assert_same_structure(gpu, fresh.export())
+
+
+def test_edit_batch_prefix_on_error(rl, oracle_mod):
+    g = random_map(16, 16, 0.1, 4)
+    gpu = make_gpu(rl, g, 8)
+    orc = oracle_mod.OracleCddt(g, 8)
+    xy = np.array([[3, 3], [5, 5], [99, 1], [6, 6]], np.int32)
+    occ = np.array([1, 1, 1, 1], np.uint8)
+    with pytest.raises(IndexError):
+        gpu.set_occupancy_batch(xy, occ)
+    orc.set_occupancy(3, 3, True)
+    orc.set_occupancy(5, 5, True)
+    assert_same_structure(gpu, orc.export())
+
+
+def test_snapshot_roundtrip_and_reference_bytes(rl, oracle_mod):
+    g = random_map(20, 14, 0.12, 55)
+    gpu = make_gpu(rl, g, 16)
+    data = rl.serialize_cddt(gpu)
+    back = rl.deserialize_cddt(data)
+    assert rl.serialize_cddt(back) == data
+    assert_same_structure(back, gpu.export())
+    if oracle_mod.ref_available():
+        ref = oracle_mod.RefCddt(g, 16)
+        assert ref.serialize() == data
+        ref.prune()
+        pr = rl.deserialize_cddt(ref.serialize())
+        assert pr.pruned()
+        assert_same_structure(pr, ref.export())
+    bad = bytearray(data)
+    bad[0] ^= 0xFF
+    with pytest.raises(rl.ParseError):
+        rl.deserialize_cddt(bytes(bad))
+    with pytest.raises(rl.ParseError):
+        rl.deserialize_cddt(data[:-3])
+    with pytest.raises(rl.ParseError):
+        rl.deserialize_cddt(data + b"\0")
+    with pytest.raises(rl.ParseError):
+        rl.deserialize_cddt(b"")
+
+
+def test_maze_cfg2_build_and_casts(rl, oracle_mod, synth):
+    """Config 2 map (2000x2000 maze, theta_disc 120, max_range 500): structure
+    and 200k casts bit-exact with the oracle."""
+    import torch
+    g = synth.maze_map()
+    gpu = make_gpu(rl, g, 120, 500.0)
+    orc = oracle_mod.OracleCddt(g, 120, 500.0)
+    assert_same_structure(gpu, orc.export())
+    qx, qy, qt = synth.free_queries(g, 200_000, seed=21)
+    want = orc.cast_batch(qx, qy, qt)
+    got = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
+    torch.cuda.synchronize()
+    assert np.array_equal(host(got), want["out32"])
