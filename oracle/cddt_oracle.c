@@ -356,6 +356,12 @@ static inline void touch(sector_set *ss, int space, uint64_t byte) {
   if (ss->n < 512) ss->s[ss->n++] = key;
 }
 
+/* ---- optional work counters (single-threaded profiling of the algorithm) ---- */
+static long g_stats[8];
+void orc_stats_reset(void) { memset(g_stats, 0, sizeof g_stats); }
+void orc_stats_get(long *out) { memcpy(out, g_stats, sizeof g_stats); }
+enum { ST_QUERIES, ST_NEAR, ST_WALK_STEPS, ST_CANDS, ST_LAND_HIT, ST_WINDOWS, ST_PLACES, ST_SEARCH };
+
 /* ---- RayWalker, proj/include/rangelib/detail/ray_walker.hpp:21-104 ---- */
 typedef struct {
   const orc_cddt *c;
@@ -370,6 +376,7 @@ static inline double boundary_t(double d, double o, int c) {
   return INFINITY;
 }
 static void w_place(walker *w, double t) {
+  g_stats[ST_PLACES]++;
   w->t = t;
   double px = w->ox + t * w->dx, py = w->oy + t * w->dy;
   w->cx = (int)floor(px);
@@ -416,6 +423,7 @@ static double w_scan_to(walker *w, double lim) {
     if (at(w->c, w->cx, w->cy)) return w->t;
     double tn = w->tnx < w->tny ? w->tnx : w->tny;
     if (tn > lim) return W_NONE;
+    g_stats[ST_WALK_STEPS]++;
     w_advance(w);
   }
 }
@@ -430,6 +438,7 @@ double orc_directional_cast(const orc_cddt *c, double x, double y, int a, int32_
                             int64_t *res_row, int32_t *res_idx, int *sectors) {
   sector_set ssv, *ss = sectors ? &ssv : NULL;
   if (ss) ss->n = 0;
+  g_stats[ST_QUERIES]++;
   int32_t h_ = -1;
   int64_t rr = -1;
   int32_t ri = -1;
@@ -458,6 +467,7 @@ double orc_directional_cast(const orc_cddt *c, double x, double y, int a, int32_
     walker wk;
     int have_walker = 0;
     if (!c->clear[(size_t)cyi * c->w + cxi]) {
+      g_stats[ST_NEAR]++;
       w_init(&wk, c, x, y, dx, dy, ss);
       have_walker = 1;
       double r = w_scan_to(&wk, K_NEAR_FIELD);
@@ -493,7 +503,9 @@ double orc_directional_cast(const orc_cddt *c, double x, double y, int a, int32_
     }
     long idx = forward ? (long)first : (long)first - 1;
     long step = forward ? 1 : -1;
+    g_stats[ST_SEARCH] += bin->n;
     for (; idx >= 0 && idx < (long)bin->n; idx += step) {
+      g_stats[ST_CANDS]++;
       touch(ss, 2, (zbase + (uint64_t)idx) * 4);
       double v = (double)bin->v[idx];
       double d = forward ? v - xq : xq - v;
@@ -506,6 +518,7 @@ double orc_directional_cast(const orc_cddt *c, double x, double y, int a, int32_
             fy < 1.0 - K_LATTICE_EPS) {
           touch(ss, 0, (uint64_t)hy * c->w + hx);
           if (at(c, hx, hy)) {
+            g_stats[ST_LAND_HIT]++;
             rr = (int64_t)grow;
             ri = (int32_t)idx;
             result = d;
@@ -518,6 +531,7 @@ double orc_directional_cast(const orc_cddt *c, double x, double y, int a, int32_
         w_init(&wk, c, x, y, dx, dy, ss);
         have_walker = 1;
       }
+      g_stats[ST_WINDOWS]++;
       w_seek(&wk, d - K_VERIFY_HALF);
       double r = w_scan_to(&wk, d + K_VERIFY_HALF);
       if (r == W_EXIT) break;

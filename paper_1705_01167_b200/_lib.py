@@ -9,8 +9,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
+import os
+
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "librl_cddt.so"
+# RL_CDDT_LIB selects an alternative in-tree build (kernel variants for A/B timing)
+LIB_PATH = Path(os.environ.get("RL_CDDT_LIB", str(_PKG / "librl_cddt.so")))
 
 RL_OK, RL_EINVAL, RL_ELOGIC, RL_ERANGE, RL_ECUDA, RL_ENOMEM, RL_EDEGENERATE, RL_EPARSE = range(8)
 

@@ -55,28 +55,32 @@ def _run(cmd: list[str], log: Path | None = None) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (exit {r.returncode})")
 
 
-def build_cuda(force: bool = False) -> Path:
+def build_cuda(force: bool = False, defines: tuple[str, ...] = (), out: Path | None = None) -> Path:
+    """Build librl_cddt.so (or, with `defines`, a variant library at `out`)."""
+    lib = out or LIB
     cu = sorted(CSRC.glob("*.cu"))
     hdrs = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
-    if not force and not _stale(LIB, cu + hdrs + [Path(__file__)]):
-        return LIB
+    if not force and not _stale(lib, cu + hdrs + [Path(__file__)]):
+        return lib
     nvcc = _nvcc()
-    OBJ.mkdir(exist_ok=True)
+    objdir = OBJ if not defines else OBJ / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    objdir.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
 
     def one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
+        obj = objdir / (src.stem + ".o")
         if force or _stale(obj, [src] + hdrs + [Path(__file__)]):
-            _run([nvcc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)],
-                 OBJ / (src.stem + ".ptxas.log"))
+            _run([nvcc, *ARCH, *NVCC_FLAGS, *dflags, "-I", str(INCLUDE), "-c", str(src), "-o",
+                  str(obj)], objdir / (src.stem + ".ptxas.log"))
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(cu))) as ex:
         objs = list(ex.map(one, cu))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     _run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lrt",
           "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 def build_synth(force: bool = False) -> Path:

@@ -33,12 +33,17 @@ struct __align__(32) SliceParam {
 };
 
 // Read-only view of one device-resident structure, passed by value.
+// Occupancy for queries lives in 8x8-cell tiles: tiles[(y>>3)*tw + (x>>3)] =
+// {occupied bits, clear bits}, bit (y&7)*8 + (x&7). A ray walk crosses a tile
+// boundary every ~8 cells, so one 8-byte load serves several DDA steps.
 struct CddtView {
-  const uint8_t* __restrict__ flags;      // w*h
+  const uint8_t* __restrict__ flags;      // w*h (build / update bookkeeping)
+  const ulonglong2* __restrict__ tiles;   // tw*th occupancy + clear tiles
+  int tw;
   const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
   const float* __restrict__ zp;           // zero points, ascending per row
   const SliceParam* __restrict__ slices;  // S
-  const double2* __restrict__ dirs;       // K (cos, sin), axis-snapped (cddt.cpp:30-42)
+  const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
   int w, h, K, S;
   double max_range;
 };
@@ -61,21 +66,64 @@ __device__ __forceinline__ int direction_index(double theta, int K) {  // raycas
   return (int)i;
 }
 
-__device__ __forceinline__ bool occ_at(const CddtView& c, int x, int y) {
-  return (__ldg(c.flags + (size_t)y * c.w + x) & kOcc) != 0;
+__device__ __forceinline__ int tile_of(const CddtView& c, int x, int y) {
+  return (y >> 3) * c.tw + (x >> 3);
 }
+__device__ __forceinline__ int bit_of(int x, int y) { return ((y & 7) << 3) | (x & 7); }
+
+#ifndef RL_TILES
+#define RL_TILES 0
+#endif
+
+// Register-resident copy of the last occupancy tile touched by a query.
+struct OccCache {
+  int tile = -1;
+  unsigned long long word = 0;
+  __device__ __forceinline__ bool occ(const CddtView& c, int x, int y) {
+#if !RL_TILES
+    return (__ldg(c.flags + (size_t)y * c.w + x) & kOcc) != 0;
+#endif
+    const int t = tile_of(c, x, y);
+    if (t != tile) {
+      tile = t;
+      word = __ldg(&c.tiles[t].x);
+    }
+    return (word >> bit_of(x, y)) & 1ull;
+  }
+};
 __device__ __forceinline__ bool in_bounds(const CddtView& c, int x, int y) {
   return x >= 0 && x < c.w && y >= 0 && y < c.h;
 }
 
-__device__ __forceinline__ double boundary_t(double d, double o, int cc) {  // ray_walker.hpp:75-79
-  if (d > 0) return ((double)cc + 1.0 - o) / d;
-  if (d < 0) return ((double)cc - o) / d;
+#ifndef RL_FAST_DIV
+#define RL_FAST_DIV 1
+#endif
+
+// a / d correctly rounded, given r = RN(1/d) (host-computed per direction):
+// q0 = RN(a r) is within one ulp of a/d and the FMA residual a - d q0 is
+// exact, so RN(q0 + (a - d q0) r) = RN(a/d) (Markstein's theorem; valid here
+// because |a| <= grid extent and |d| >= sin(2pi/theta_disc) keep every
+// intermediate far from overflow and the subnormal range). Replaces the
+// ~30-instruction IEEE division sequence with 3 FP64 operations; checked
+// bit-for-bit against IEEE division by tests/test_fast_div.py.
+__device__ __forceinline__ double div_rn(double a, double d, double r) {
+#if RL_FAST_DIV
+  const double q0 = __dmul_rn(a, r);
+  const double e = fma(-d, q0, a);
+  return fma(e, r, q0);
+#else
+  return a / d;
+#endif
+}
+
+__device__ __forceinline__ double boundary_t(double d, double o, int cc, double r) {  // ray_walker.hpp:75-79
+  if (d > 0) return div_rn((double)cc + 1.0 - o, d, r);
+  if (d < 0) return div_rn((double)cc - o, d, r);
   return __longlong_as_double(0x7ff0000000000000ll);
 }
 
 struct Walker {
-  double ox, oy, dx, dy, t, tnx, tny;
+  double ox, oy, dx, dy, rx, ry, t, tnx, tny;
   int cx, cy;
 
   __device__ __forceinline__ void place(double tt) {  // ray_walker.hpp:62-73
@@ -85,14 +133,16 @@ struct Walker {
     cy = (int)floor(py);
     if (dx < 0 && px == (double)cx) cx--;
     if (dy < 0 && py == (double)cy) cy--;
-    tnx = boundary_t(dx, ox, cx);
-    tny = boundary_t(dy, oy, cy);
+    tnx = boundary_t(dx, ox, cx, rx);
+    tny = boundary_t(dy, oy, cy, ry);
   }
-  __device__ __forceinline__ void init(double x, double y, double ddx, double ddy) {
+  __device__ __forceinline__ void init(double x, double y, const double4& dir) {
     ox = x;
     oy = y;
-    dx = ddx;
-    dy = ddy;
+    dx = dir.x;
+    dy = dir.y;
+    rx = dir.z;
+    ry = dir.w;
     place(0.0);
   }
   __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
@@ -103,28 +153,87 @@ struct Walker {
       t = tnx;
       cx += dx > 0 ? 1 : -1;
       cy += dy > 0 ? 1 : -1;
-      tnx = boundary_t(dx, ox, cx);
-      tny = boundary_t(dy, oy, cy);
+      tnx = boundary_t(dx, ox, cx, rx);
+      tny = boundary_t(dy, oy, cy, ry);
     } else if (tnx < tny) {
       t = tnx;
       cx += dx > 0 ? 1 : -1;
-      tnx = boundary_t(dx, ox, cx);
+      tnx = boundary_t(dx, ox, cx, rx);
     } else {
       t = tny;
       cy += dy > 0 ? 1 : -1;
-      tny = boundary_t(dy, oy, cy);
+      tny = boundary_t(dy, oy, cy, ry);
     }
   }
-  __device__ __forceinline__ double scan_to(const CddtView& c, double lim) {  // :51-59
+  __device__ __forceinline__ double scan_to(const CddtView& c, OccCache& oc, double lim) {  // :51-59
     for (;;) {
       if (!in_bounds(c, cx, cy)) return kWalkExit;
-      if (occ_at(c, cx, cy)) return t;
+      if (oc.occ(c, cx, cy)) return t;
       double tn = tnx < tny ? tnx : tny;
       if (tn > lim) return kWalkNone;
       advance();
     }
   }
 };
+
+#ifndef RL_SEARCH
+#define RL_SEARCH 8
+#endif
+
+// Number of leading elements e of v[0, n) with pred(e): e <= xq (forward,
+// i.e. !(xq < e), upper_bound) or e < xq (backward, lower_bound).
+__device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v, uint32_t n,
+                                                    double xq, bool forward) {
+#if RL_SEARCH == 8
+  // 8-way search: each level issues 7 independent pivot loads, so a row of
+  // length n costs ~log8(n) dependent load rounds instead of log2(n).
+  uint32_t base = 0, len = n;  // partition point lies in [base, base + len]
+  while (len > 8) {
+    const uint32_t s = len >> 3;
+    float pv[7];
+#pragma unroll
+    for (int j = 0; j < 7; j++) pv[j] = __ldg(v + base + (j + 1) * s - 1);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 7; j++) {
+      const double e = (double)pv[j];
+      cnt += (forward ? !(xq < e) : (e < xq)) ? 1u : 0u;
+    }
+    if (cnt == 7) {
+      base += 7 * s;
+      len -= 7 * s;
+    } else {
+      base += cnt * s;
+      len = s - 1;
+    }
+  }
+  float tv[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) tv[j] = (uint32_t)j < len ? __ldg(v + base + j) : 0.0f;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const double e = (double)tv[j];
+    cnt += ((uint32_t)j < len && (forward ? !(xq < e) : (e < xq))) ? 1u : 0u;
+  }
+  return base + cnt;
+#else
+  // libstdc++'s halving sequence
+  uint32_t first = 0, len = n;
+  while (len > 0) {
+    uint32_t half = len >> 1, mid = first + half;
+    double vm = (double)__ldg(v + mid);
+    bool right = forward ? !(xq < vm) : (vm < xq);
+    if (right) {
+      first = mid + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  return first;
+#endif
+}
 
 // Outcome of one query beyond the range: the occupied cell that settled it
 // and the resolving zero point (what MarkSink::mark receives, cddt.cpp:249,259).
@@ -142,11 +251,25 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   o.res_g = 0;
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) return c.max_range;
+  OccCache oc;
+#if RL_TILES
+  oc.tile = tile_of(c, cxi, cyi);
+  const ulonglong2 t0 = __ldg(c.tiles + oc.tile);
+  oc.word = t0.x;
+  const int b0 = bit_of(cxi, cyi);
+  if ((t0.x >> b0) & 1ull) {
+    o.hit = cyi * c.w + cxi;
+    return 0.0;
+  }
+  const bool clear0 = (t0.y >> b0) & 1ull;
+#else
   const uint8_t f0 = __ldg(c.flags + (size_t)cyi * c.w + cxi);
   if (f0 & kOcc) {
     o.hit = cyi * c.w + cxi;
     return 0.0;
   }
+  const bool clear0 = (f0 & kClear) != 0;
+#endif
   const bool forward = a < c.S;
   const int s = forward ? a : a - c.S;
   const SliceParam sp = c.slices[s];
@@ -155,15 +278,15 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   int row = (int)yq;
   if (row < 0) row = 0;
   if (row >= sp.bin_count) row = sp.bin_count - 1;
-  const double2 dir = __ldg(c.dirs + a);
+  const double4 dir = c.dirs[a];
   const double dx = dir.x, dy = dir.y;
 
   Walker wk;
   bool have_walker = false;
-  if (!(f0 & kClear)) {
-    wk.init(x, y, dx, dy);
+  if (!clear0) {
+    wk.init(x, y, dir);
     have_walker = true;
-    double r = wk.scan_to(c, kNearField);
+    double r = wk.scan_to(c, oc, kNearField);
     if (r >= 0.0) {
       o.hit = wk.cy * c.w + wk.cx;
       return (c.max_range < r) ? c.max_range : r;
@@ -177,19 +300,9 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
   const float* __restrict__ v = c.zp + lo;
   // std::upper_bound (forward, xq < double(v)) / std::lower_bound (backward,
-  // double(v) < xq) with libstdc++'s halving sequence (cddt.hpp:106-131)
-  uint32_t first = 0, len = hi - lo;
-  while (len > 0) {
-    uint32_t half = len >> 1, mid = first + half;
-    double vm = (double)__ldg(v + mid);
-    bool right = forward ? !(xq < vm) : (vm < xq);
-    if (right) {
-      first = mid + 1;
-      len -= half + 1;
-    } else {
-      len = half;
-    }
-  }
+  // double(v) < xq): the partition point of a monotone predicate over the
+  // sorted row (cddt.hpp:106-131); any search order yields the same index.
+  const uint32_t first = partition_point(v, hi - lo, xq, forward);
   const int n = (int)(hi - lo);
   int idx = forward ? (int)first : (int)first - 1;
   const int step = forward ? 1 : -1;
@@ -203,7 +316,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
       const int hx = (int)px, hy = (int)py;
       const double fx = px - (double)hx, fy = py - (double)hy;
       if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
-          fy < 1.0 - kLatticeEps && occ_at(c, hx, hy)) {
+          fy < 1.0 - kLatticeEps && oc.occ(c, hx, hy)) {
         o.hit = hy * c.w + hx;
         o.res_g = g;
         o.res_idx = idx;
@@ -213,11 +326,11 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     }
     // verification window around the candidate (cddt.cpp:254-261)
     if (!have_walker) {
-      wk.init(x, y, dx, dy);
+      wk.init(x, y, dir);
       have_walker = true;
     }
     wk.seek(d - kVerifyHalf);
-    double r = wk.scan_to(c, d + kVerifyHalf);
+    double r = wk.scan_to(c, oc, d + kVerifyHalf);
     if (r == kWalkExit) break;
     if (r < 0.0) continue;
     o.hit = wk.cy * c.w + wk.cx;

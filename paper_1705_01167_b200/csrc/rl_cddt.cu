@@ -7,7 +7,7 @@
 //                       slice s owns global rows [row_base[s], row_base[s]+bin_count)
 //   zp[zero_points] f32 zero points, ascending within each row
 //   slices[S]       SliceParam (cos, sin, y_offset, bin_count, row_base)
-//   dirs[K]         double2 direction lattice, host glibc cos/sin, axis snapped
+//   dirs[K]         double4 direction lattice (cos, sin, 1/cos, 1/sin), host glibc, axis snapped
 //
 // Construction (Cddt::Cddt, proj/src/cddt.cpp:136-171) is a count -> scan ->
 // scatter -> segmented sort pipeline; pruning (cddt.cpp:281-330) is a marking
@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "cddt_cast_sm.cuh"
 #include "rl_common.cuh"
 
 namespace rl {
@@ -95,11 +96,14 @@ int init_geometry(rl_cddt* c) {
   c->rows = base;
   RL_TRY(c->d_slices.alloc(c->S));
   RL_TRY(c->d_dirs.alloc(c->K));
-  std::vector<double2> dirs(c->K);
-  for (int a = 0; a < c->K; a++) dirs[a] = make_double2(c->dcos[a], c->dsin[a]);
+  // reciprocals for the walker's boundary divisions (cddt_device.cuh div_rn)
+  std::vector<double4> dirs(c->K);
+  for (int a = 0; a < c->K; a++)
+    dirs[a] = make_double4(c->dcos[a], c->dsin[a], c->dcos[a] != 0.0 ? 1.0 / c->dcos[a] : 0.0,
+                           c->dsin[a] != 0.0 ? 1.0 / c->dsin[a] : 0.0);
   RL_CK(cudaMemcpyAsync(c->d_slices.p, c->slices.data(), sizeof(SliceParam) * c->S,
                         cudaMemcpyHostToDevice, c->stream));
-  RL_CK(cudaMemcpyAsync(c->d_dirs.p, dirs.data(), sizeof(double2) * c->K, cudaMemcpyHostToDevice,
+  RL_CK(cudaMemcpyAsync(c->d_dirs.p, dirs.data(), sizeof(double4) * c->K, cudaMemcpyHostToDevice,
                         c->stream));
   RL_CK(cudaStreamSynchronize(c->stream));
   return RL_OK;
@@ -135,6 +139,40 @@ __global__ void k_flags(const uint8_t* __restrict__ grid, uint8_t* __restrict__ 
     if (occ && any_free_or_oob_nb) f |= kMember;
     flags[i] = f;
   }
+}
+
+// Query tiles: 8x8 cells per tile, occupied and clear bits (cddt_device.cuh).
+__global__ void k_tiles(const uint8_t* __restrict__ flags, int w, int h, int tw, int th,
+                        ulonglong2* __restrict__ tiles) {
+  const int n = tw * th;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int x0 = (t % tw) * 8, y0 = (t / tw) * 8;
+    unsigned long long occ = 0, clr = 0;
+    for (int dy = 0; dy < 8; dy++) {
+      const int y = y0 + dy;
+      if (y >= h) break;
+      for (int dx = 0; dx < 8; dx++) {
+        const int x = x0 + dx;
+        if (x >= w) break;
+        const uint8_t f = flags[size_t(y) * w + x];
+        const int b = dy * 8 + dx;
+        if (f & kOcc) occ |= 1ull << b;
+        if (f & kClear) clr |= 1ull << b;
+      }
+    }
+    tiles[t] = make_ulonglong2(occ, clr);
+  }
+}
+
+int refresh_tiles(rl_cddt* c) {
+  c->tw = (c->w + 7) / 8;
+  c->th = (c->h + 7) / 8;
+  const size_t n = size_t(c->tw) * c->th;
+  if (c->tiles.n != n) RL_TRY(c->tiles.alloc(n));
+  k_tiles<<<int(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 16)), 256, 0, c->stream>>>(
+      c->flags.p, c->w, c->h, c->tw, c->th, c->tiles.p);
+  RL_CK(cudaGetLastError());
+  return RL_OK;
 }
 
 // Compact member cells into an (unordered) edge list; warp-aggregated atomics.
@@ -289,6 +327,7 @@ int build_structure(rl_cddt* c) {
     RL_CK(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, unsorted.p, c->zp.p, int(total),
                                              int(rows), c->row_off.p, c->row_off.p + 1, st));
   }
+  RL_TRY(refresh_tiles(c));
   // host membership mirror
   c->member_h.assign(wh, 0);
   {
@@ -302,24 +341,92 @@ int build_structure(rl_cddt* c) {
 
 // ---------------------------------------------------------------------------
 // K3: batched casts, one thread per query, grid-stride.
+#ifndef RL_STREAM_IO
+#define RL_STREAM_IO 1
+#endif
+#ifndef RL_GRID_PER_SM
+#define RL_GRID_PER_SM 0  // 0: one full wave from the occupancy calculator
+#endif
+#ifndef RL_CAST_MINB
+#define RL_CAST_MINB 4  // resident 256-thread CTAs per SM the register budget targets
+#endif
 template <class T>
-__global__ void __launch_bounds__(256) k_cast(CddtView c, const T* __restrict__ qx,
+__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T* __restrict__ qx,
                                               const T* __restrict__ qy, const T* __restrict__ qt,
                                               T* __restrict__ out, int32_t* __restrict__ hit,
                                               int64_t* __restrict__ res_row,
                                               int32_t* __restrict__ res_idx, size_t n) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
+#if RL_STREAM_IO
+    // query streams are touched once: evict-first so the structure stays in L2
+    const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
+    const double th = normalize_angle_2pi(double(__ldcs(qt + i)));  // RayQuery ctor, raycast.hpp:47
+#else
     const double x = double(qx[i]), y = double(qy[i]);
-    const double th = normalize_angle_2pi(double(qt[i]));  // RayQuery ctor, raycast.hpp:47
+    const double th = normalize_angle_2pi(double(qt[i]));
+#endif
     const int a = direction_index(th, c.K);
     CastOut o;
     const double r = directional_cast(c, x, y, a, o);
+#if RL_STREAM_IO
+    if (out) __stcs(out + i, T(r));
+#else
     if (out) out[i] = T(r);
+#endif
     if (hit) hit[i] = o.hit;
     if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
     if (res_idx) res_idx[i] = o.res_idx;
   }
+}
+
+#ifndef RL_CAST_SM
+#define RL_CAST_SM 0
+#endif
+// K3 (state-machine form, cddt_cast_sm.cuh)
+template <class T, bool HIT, bool RES>
+__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast_sm(
+    CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
+    T* __restrict__ out, int32_t* __restrict__ hit, int64_t* __restrict__ res_row,
+    int32_t* __restrict__ res_idx, size_t n) {
+  cast_stream<T, HIT, RES>(c, qx, qy, qt, out, hit, res_row, res_idx,
+                           blockIdx.x * size_t(blockDim.x) + threadIdx.x,
+                           size_t(gridDim.x) * blockDim.x, n);
+}
+
+template <class T, bool HIT, bool RES>
+static int sm_blocks(size_t n) {
+  static int per_sm = RL_GRID_PER_SM;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast_sm<T, HIT, RES>, 256, 0);
+    if (per_sm <= 0) per_sm = 1;
+  }
+  size_t b = (n + 255) / 256;
+  return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * per_sm)));
+}
+
+template <class T>
+static int cast_blocks(size_t n);
+
+// Dispatch of the batched cast kernels for the device-pointer entry points.
+template <class T>
+static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out, int32_t* hit,
+                        int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
+#if RL_CAST_SM
+  const CddtView v = c->view();
+  if (rr || ri) {
+    k_cast_sm<T, true, true><<<sm_blocks<T, true, true>(n), 256, 0, st>>>(v, x, y, t, out, hit,
+                                                                         rr, ri, n);
+  } else if (hit) {
+    k_cast_sm<T, true, false><<<sm_blocks<T, true, false>(n), 256, 0, st>>>(v, x, y, t, out, hit,
+                                                                           rr, ri, n);
+  } else {
+    k_cast_sm<T, false, false><<<sm_blocks<T, false, false>(n), 256, 0, st>>>(v, x, y, t, out,
+                                                                             hit, rr, ri, n);
+  }
+#else
+  k_cast<T><<<cast_blocks<T>(n), 256, 0, st>>>(c->view(), x, y, t, out, hit, rr, ri, n);
+#endif
 }
 
 __global__ void k_directional(CddtView c, const double* __restrict__ x,
@@ -341,11 +448,22 @@ __global__ void k_single(CddtView c, double x, double y, double theta, int pair,
   if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
 }
 
+// One full wave: every SM holds as many 256-thread CTAs as registers allow
+// and the grid-stride loop spreads the queries evenly (no partial last wave).
+template <class T>
 static int cast_blocks(size_t n) {
-  // enough resident warps to cover the dependent-load latency; grid-stride beyond
+  static int per_sm = RL_GRID_PER_SM;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast<T>, 256, 0);
+    if (per_sm <= 0) per_sm = 1;
+  }
   size_t b = (n + 255) / 256;
-  size_t cap = size_t(sm_count()) * 8;
+  size_t cap = size_t(sm_count()) * per_sm;
   return int(std::max<size_t>(1, std::min(b, cap)));
+}
+static int dir_blocks(size_t n) {
+  size_t b = (n + 255) / 256;
+  return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * 8)));
 }
 
 // ---------------------------------------------------------------------------
@@ -519,6 +637,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     DeviceGuard guard(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     c->flags.release();
+    c->tiles.release();
     c->row_off.release();
     c->zp.release();
     c->d_slices.release();
@@ -594,8 +713,7 @@ int rl_cddt_cast_batch(rl_cddt* c, const float* x, const float* y, const float* 
   if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  k_cast<float><<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, theta, out,
-                                                                     hit, nullptr, nullptr, n);
+  launch_cast<float>(c, x, y, theta, out, hit, nullptr, nullptr, n, pick_stream(c, stream));
   return finish(c, stream);
 }
 
@@ -605,8 +723,7 @@ int rl_cddt_cast_batch_f64(rl_cddt* c, const double* x, const double* y, const d
   if (!c || (n && (!x || !y || !theta))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  k_cast<double><<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(
-      c->view(), x, y, theta, out, hit, res_row, res_idx, n);
+  launch_cast<double>(c, x, y, theta, out, hit, res_row, res_idx, n, pick_stream(c, stream));
   return finish(c, stream);
 }
 
@@ -615,7 +732,7 @@ int rl_cddt_directional_batch(rl_cddt* c, const double* x, const double* y, cons
   if (!c || (n && (!x || !y || !a || !out))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  k_directional<<<cast_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, a, out, n);
+  k_directional<<<dir_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, a, out, n);
   return finish(c, stream);
 }
 
@@ -663,8 +780,7 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
     RL_CK(cudaMemcpyAsync(dx, x + off, m * 4, cudaMemcpyHostToDevice, l.s));
     RL_CK(cudaMemcpyAsync(dy, y + off, m * 4, cudaMemcpyHostToDevice, l.s));
     RL_CK(cudaMemcpyAsync(dt, theta + off, m * 4, cudaMemcpyHostToDevice, l.s));
-    k_cast<float><<<cast_blocks(m), 256, 0, l.s>>>(c->view(), dx, dy, dt, dout, nullptr, nullptr,
-                                                    nullptr, m);
+    launch_cast<float>(c, dx, dy, dt, dout, nullptr, nullptr, nullptr, m, l.s);
     RL_CK(cudaGetLastError());
     RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
   }

@@ -111,16 +111,20 @@ struct rl_cddt {
   std::vector<uint8_t> member_h;  // host mirror: membership
 
   rl::DevBuf<uint8_t> flags;        // w*h
+  rl::DevBuf<ulonglong2> tiles;     // 8x8 occupancy/clear tiles for queries
+  int tw = 0, th = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
   rl::DevBuf<float> zp;             // capacity >= zero_points
   rl::DevBuf<rl::SliceParam> d_slices;
-  rl::DevBuf<double2> d_dirs;
+  rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
 
   rl::CddtView view() const {
     rl::CddtView v;
     v.flags = flags.p;
+    v.tiles = tiles.p;
+    v.tw = tw;
     v.row_off = row_off.p;
     v.zp = zp.p;
     v.slices = d_slices.p;
@@ -140,4 +144,5 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
   return s ? static_cast<cudaStream_t>(s) : c->stream;
 }
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
+int refresh_tiles(rl_cddt* c);          // rebuild query tiles from flags
 }  // namespace rl

@@ -228,6 +228,7 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   k_set_flags<<<blocks_for(wcells.size(), 256), 256, 0, st>>>(d_wcells.p, d_wflags.p,
                                                               int(wcells.size()), c->flags.p);
   RL_CK(cudaGetLastError());
+  RL_TRY(refresh_tiles(c));
   if (dcells.empty()) return RL_OK;
 
   // 3. delta records
