@@ -345,3 +345,69 @@ def test_maze_cfg2_build_and_casts(rl, oracle_mod, synth):
     got = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
     torch.cuda.synchronize()
     assert np.array_equal(host(got), want["out32"])
+
+
+# ---- full-size pins against hashes produced by the unmodified reference
+# (tests/golden/make_golden.py --large; config-3 PCDDT took the reference
+# 784 s single-threaded) ----
+import hashlib  # noqa: E402
+import json  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+_LARGE_PATH = Path(__file__).resolve().parent / "golden" / "large.json"
+LARGE = json.loads(_LARGE_PATH.read_text()) if _LARGE_PATH.exists() else {}
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _map_for(name, synth):
+    if name.startswith("cfg1"):
+        return synth.rect_map()
+    if name.startswith("cfg3"):
+        return synth.polygon_map()
+    return synth.maze_map()
+
+
+@pytest.mark.parametrize("name", ["cfg1_cddt", "cfg1_pcddt", "cfg2_cddt", "cfg3_cddt",
+                                  "cfg3_pcddt"])
+def test_full_size_structure_and_casts_vs_reference_hashes(rl, synth, name):
+    import torch
+    want = LARGE.get(name)
+    if want is None:
+        pytest.skip("tests/golden/large.json missing")
+    g = _map_for(name, synth)
+    c = make_gpu(rl, g, want["theta_disc"], want["max_range"], prune=want["pruned"])
+    e = c.export()
+    assert c.zero_point_count() == want["info"]["zero_points"]
+    assert c.memory_bytes() == want["info"]["memory_bytes"]
+    assert _sha(e["zp"]) == want["zp_sha"]
+    assert _sha(e["row_off"]) == want["row_off_sha"]
+    assert _sha(e["membership"]) == want["membership_sha"]
+    qx, qy, qt = synth.free_queries(g, want["queries"], seed=want["query_seed"])
+    out = torch.empty(qx.size, dtype=torch.float64, device="cuda")
+    c.cast_batch_f64(*(dev(a.astype(np.float64)) for a in (qx, qy, qt)), out=out)
+    o32 = c.cast_batch(dev(qx), dev(qy), dev(qt))
+    torch.cuda.synchronize()
+    assert _sha(host(out)) == want["casts_sha"]
+    assert _sha(host(o32)) == want["casts_f32_sha"]
+
+
+def test_full_size_edit_rounds_vs_reference_hashes(rl, synth):
+    """Config 5: 2000x2000 maze, theta_disc 108, rounds of 50 random 3x3
+    insert/remove blocks; zero points bit-exact with the reference after every
+    round (hashes from the reference's sequential set_occupancy)."""
+    rounds = LARGE.get("cfg5_rounds")
+    if not rounds:
+        pytest.skip("tests/golden/large.json missing")
+    g = synth.maze_map()
+    c = make_gpu(rl, g, 108, 0.0)
+    for rd in rounds:
+        xy, occ = synth.block_edits(2000, 2000, 50, seed=rd["seed"])
+        c.set_occupancy_batch(xy, occ)
+        e = c.export()
+        assert c.zero_point_count() == rd["zero_points"]
+        assert _sha(e["zp"]) == rd["zp_sha"]
+        assert _sha(e["row_off"]) == rd["row_off_sha"]
+        assert _sha(e["membership"]) == rd["membership_sha"]
