@@ -157,6 +157,64 @@ int rl_sensor_update(rl_cddt *c, const double *px, const double *py, const doubl
                      const float *table, int32_t zdim, double inv_res, double *logw, double *weight,
                      void *stream);
 
+/* ---- particle-filter step (Mcl::step, mcl.cpp:189-201), stage by stage so a
+ * multi-GPU driver can place its collectives between stages. All pointers are
+ * device pointers; `stream` as above. Random numbers are counter-based
+ * (Philox4x32-10 keyed by seed, counter = (particle index, draw, iteration)),
+ * so a particle's noise does not depend on how particles are sharded. ---- */
+
+/* MotionNoise (mcl.hpp:18-27). */
+typedef struct {
+  double trans_per_trans, trans_per_rot, rot_per_rot, rot_per_trans;
+} rl_motion_noise_t;
+
+/* motion_update (mcl.cpp:42-56): sigma_t = a|trans| + b|rot|, sigma_r =
+ * c|rot| + d|trans| (floored at 1e-12), per particle three normals (rdx, rdy,
+ * rdtheta) applied in the robot frame. index_offset is the global index of
+ * particle 0 of this shard. */
+int rl_motion_update(double *x, double *y, double *theta, size_t n, uint64_t index_offset,
+                     double dx, double dy, double dtheta, const rl_motion_noise_t *noise,
+                     uint64_t seed, uint64_t iteration, void *stream);
+
+/* Log-weights only (the first half of sensor_update): logw[i] = sum over beams
+ * of log likelihood, beams in order. Arguments as rl_sensor_update. */
+int rl_sensor_logw(rl_cddt *c, const double *px, const double *py, const double *pt, size_t n,
+                   const double *scan, int32_t nbeams, double fov, const rl_beam_params_t *params,
+                   const float *table, int32_t zdim, double inv_res, double *logw, void *stream);
+
+/* out[0] = max over logw[0, n) (device). */
+int rl_pf_max(const double *logw, size_t n, double *out, void *stream);
+
+/* w[i] = exp(logw[i] - *gmax); moments[0..9] = {sum w, sum w x, sum w y,
+ * sum w cos t, sum w sin t, n, sum x, sum y, sum cos t, sum sin t} over this
+ * shard (deterministic order). */
+int rl_pf_weights(const double *logw, const double *gmax, const double *x, const double *y,
+                  const double *theta, size_t n, double *w, double *moments, void *stream);
+
+/* Normalise with the global sum moments[0] (mcl.cpp:108-119): w /= sum, or
+ * w = 1/n_total and *degenerate = 1 when the sum is zero or not finite. */
+int rl_pf_normalize(double *w, size_t n, const double *moments, uint64_t n_total,
+                    int32_t *degenerate, void *stream);
+
+/* resample_low_variance (mcl.cpp:122-142) over the full set (x, y, theta, w)
+ * of n particles: r = U[0, 1/n) from the counter RNG, slot m takes the first
+ * particle whose cumulative weight reaches r + m/n. Writes the slots
+ * [out_begin, out_begin + out_count) with weight 1/n. */
+int rl_resample_low_variance(const double *x, const double *y, const double *theta,
+                             const double *w, size_t n, size_t out_begin, size_t out_count,
+                             double *ox, double *oy, double *otheta, double *ow, uint64_t seed,
+                             uint64_t iteration, void *stream);
+
+/* Whole Mcl::step on one GPU: motion -> sensor -> estimate -> resample, with
+ * the particle arrays updated in place. estimate (host, 3 doubles) receives
+ * the weighted mean pose (Mcl::estimate, mcl.cpp:176-187) before resampling;
+ * returns RL_EDEGENERATE when the weights were reset. */
+int rl_mcl_step(rl_cddt *c, double *x, double *y, double *theta, double *w, size_t n,
+                double odo_dx, double odo_dy, double odo_dtheta, const double *scan,
+                int32_t nbeams, double fov, const rl_motion_noise_t *noise,
+                const rl_beam_params_t *params, const float *table, int32_t zdim, double inv_res,
+                uint64_t seed, uint64_t iteration, double *estimate, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,11 @@ class rl_beam_params_t(C.Structure):
                 ("w_hit", "w_short", "w_max", "w_rand", "sigma_hit", "lambda_short", "z_max")]
 
 
+class rl_motion_noise_t(C.Structure):
+    _fields_ = [(n, C.c_double) for n in
+                ("trans_per_trans", "trans_per_rot", "rot_per_rot", "rot_per_trans")]
+
+
 _P = C.c_void_p
 _SIG = {
     "rl_last_error": (C.c_char_p, []),
@@ -71,6 +76,20 @@ _SIG = {
     "rl_sensor_update": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,
                                    C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double, _P,
                                    _P, _P]),
+    "rl_sensor_logw": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,
+                                 C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double, _P, _P]),
+    "rl_motion_update": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_uint64, C.c_double, C.c_double,
+                                   C.c_double, C.POINTER(rl_motion_noise_t), C.c_uint64,
+                                   C.c_uint64, _P]),
+    "rl_pf_max": (C.c_int, [_P, C.c_size_t, _P, _P]),
+    "rl_pf_weights": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, _P, _P, _P]),
+    "rl_pf_normalize": (C.c_int, [_P, C.c_size_t, _P, C.c_uint64, _P, _P]),
+    "rl_resample_low_variance": (C.c_int, [_P, _P, _P, _P, C.c_size_t, C.c_size_t, C.c_size_t,
+                                           _P, _P, _P, _P, C.c_uint64, C.c_uint64, _P]),
+    "rl_mcl_step": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, C.c_double, C.c_double, C.c_double,
+                              _P, C.c_int32, C.c_double, C.POINTER(rl_motion_noise_t),
+                              C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double,
+                              C.c_uint64, C.c_uint64, _P, _P]),
 }
 
 _lib = None

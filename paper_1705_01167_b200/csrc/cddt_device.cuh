@@ -54,14 +54,24 @@ __host__ __device__ __forceinline__ double fmax_std(double a, double b) { return
 __device__ __forceinline__ long iround(double v) { return (long)ceil(v - 0.5); }  // raycast.hpp:17
 
 __device__ __forceinline__ double normalize_angle_2pi(double t) {  // raycast.hpp:20-25
+  if (t >= 0.0 && t < kTwoPi) return t;  // fmod(t, 2pi) == t exactly here
   t = fmod(t, kTwoPi);
   if (t < 0) t += kTwoPi;
   if (t >= kTwoPi) t = 0.0;
   return t;
 }
 
+__device__ __forceinline__ double div_rn(double a, double d, double r);
+constexpr double kInvTwoPi = 1.0 / kTwoPi;  // RN(1/2pi), folded at compile time
+
 __device__ __forceinline__ int direction_index(double theta, int K) {  // raycast.hpp:36-40
-  long i = iround(theta * (double)K / kTwoPi) % K;
+  // iround(theta * K / 2pi) % K; the quotient is the correctly rounded one
+  const double v = ceil(div_rn(theta * (double)K, kTwoPi, kInvTwoPi) - 0.5);
+  if (v >= 0.0 && v <= (double)K) {  // theta in [0, 2pi): plain range, no modulo
+    const int i = (int)v;
+    return i == K ? 0 : i;
+  }
+  long i = (long)v % K;
   if (i < 0) i += K;
   return (int)i;
 }
@@ -92,7 +102,7 @@ struct OccCache {
   }
 };
 __device__ __forceinline__ bool in_bounds(const CddtView& c, int x, int y) {
-  return x >= 0 && x < c.w && y >= 0 && y < c.h;
+  return (unsigned)x < (unsigned)c.w && (unsigned)y < (unsigned)c.h;
 }
 
 #ifndef RL_FAST_DIV
@@ -106,7 +116,7 @@ __device__ __forceinline__ bool in_bounds(const CddtView& c, int x, int y) {
 // intermediate far from overflow and the subnormal range). Replaces the
 // ~30-instruction IEEE division sequence with 3 FP64 operations; checked
 // bit-for-bit against IEEE division by tests/test_fast_div.py.
-__device__ __forceinline__ double div_rn(double a, double d, double r) {
+__device__ __forceinline__ double div_rn(double a, double d, double r) {  // NOLINT
 #if RL_FAST_DIV
   const double q0 = __dmul_rn(a, r);
   const double e = fma(-d, q0, a);
@@ -177,13 +187,19 @@ struct Walker {
 };
 
 #ifndef RL_SEARCH
-#define RL_SEARCH 8
+#define RL_SEARCH 2
 #endif
 
 // Number of leading elements e of v[0, n) with pred(e): e <= xq (forward,
 // i.e. !(xq < e), upper_bound) or e < xq (backward, lower_bound).
+//
+// Comparisons run in the float domain, exactly: for a float e,
+//   double(e) <= xq  <=>  e <= RD_f32(xq)     and     double(e) < xq  <=>  e < RU_f32(xq)
+// (no float lies strictly between RD_f32(xq) and RU_f32(xq)).
 __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v, uint32_t n,
                                                     double xq, bool forward) {
+  const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
+#define RL_PRED(e) (forward ? ((e) <= xlo) : ((e) < xhi))
 #if RL_SEARCH == 8
   // 8-way search: each level issues 7 independent pivot loads, so a row of
   // length n costs ~log8(n) dependent load rounds instead of log2(n).
@@ -195,10 +211,7 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
     for (int j = 0; j < 7; j++) pv[j] = __ldg(v + base + (j + 1) * s - 1);
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 7; j++) {
-      const double e = (double)pv[j];
-      cnt += (forward ? !(xq < e) : (e < xq)) ? 1u : 0u;
-    }
+    for (int j = 0; j < 7; j++) cnt += RL_PRED(pv[j]) ? 1u : 0u;
     if (cnt == 7) {
       base += 7 * s;
       len -= 7 * s;
@@ -212,19 +225,14 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
   for (int j = 0; j < 8; j++) tv[j] = (uint32_t)j < len ? __ldg(v + base + j) : 0.0f;
   uint32_t cnt = 0;
 #pragma unroll
-  for (int j = 0; j < 8; j++) {
-    const double e = (double)tv[j];
-    cnt += ((uint32_t)j < len && (forward ? !(xq < e) : (e < xq))) ? 1u : 0u;
-  }
+  for (int j = 0; j < 8; j++) cnt += ((uint32_t)j < len && RL_PRED(tv[j])) ? 1u : 0u;
   return base + cnt;
 #else
   // libstdc++'s halving sequence
   uint32_t first = 0, len = n;
   while (len > 0) {
     uint32_t half = len >> 1, mid = first + half;
-    double vm = (double)__ldg(v + mid);
-    bool right = forward ? !(xq < vm) : (vm < xq);
-    if (right) {
+    if (RL_PRED(__ldg(v + mid))) {
       first = mid + 1;
       len -= half + 1;
     } else {
@@ -233,6 +241,7 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
   }
   return first;
 #endif
+#undef RL_PRED
 }
 
 // Outcome of one query beyond the range: the occupied cell that settled it

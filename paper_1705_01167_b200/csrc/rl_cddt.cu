@@ -350,14 +350,14 @@ int build_structure(rl_cddt* c) {
 #ifndef RL_CAST_MINB
 #define RL_CAST_MINB 4  // resident 256-thread CTAs per SM the register budget targets
 #endif
-template <class T>
+template <class T, class I, bool HIT, bool RES>
 __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T* __restrict__ qx,
                                               const T* __restrict__ qy, const T* __restrict__ qt,
                                               T* __restrict__ out, int32_t* __restrict__ hit,
                                               int64_t* __restrict__ res_row,
-                                              int32_t* __restrict__ res_idx, size_t n) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x) {
+                                              int32_t* __restrict__ res_idx, I n) {
+  for (I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); i < n;
+       i += I(gridDim.x) * I(blockDim.x)) {
 #if RL_STREAM_IO
     // query streams are touched once: evict-first so the structure stays in L2
     const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
@@ -374,10 +374,26 @@ __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T*
 #else
     if (out) out[i] = T(r);
 #endif
-    if (hit) hit[i] = o.hit;
-    if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
-    if (res_idx) res_idx[i] = o.res_idx;
+    if (HIT) hit[i] = o.hit;
+    if (RES) {
+      if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
+      if (res_idx) res_idx[i] = o.res_idx;
+    }
   }
+}
+
+// One full wave: every SM holds as many 256-thread CTAs as registers allow
+// and the grid-stride loop spreads the queries evenly (no partial last wave).
+template <class T, class I, bool HIT, bool RES>
+static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t, T* out,
+                          int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
+  static int per_sm = RL_GRID_PER_SM;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast<T, I, HIT, RES>, 256, 0);
+    if (per_sm <= 0) per_sm = 1;
+  }
+  const size_t b = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * per_sm));
+  k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
 }
 
 #ifndef RL_CAST_SM
@@ -405,9 +421,6 @@ static int sm_blocks(size_t n) {
   return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * per_sm)));
 }
 
-template <class T>
-static int cast_blocks(size_t n);
-
 // Dispatch of the batched cast kernels for the device-pointer entry points.
 template <class T>
 static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out, int32_t* hit,
@@ -425,7 +438,21 @@ static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T*
                                                                              hit, rr, ri, n);
   }
 #else
-  k_cast<T><<<cast_blocks<T>(n), 256, 0, st>>>(c->view(), x, y, t, out, hit, rr, ri, n);
+  const CddtView v = c->view();
+  const bool small = n < (size_t(1) << 31);
+  if (rr || ri) {
+    launch_k_cast<T, size_t, true, true>(v, x, y, t, out, hit, rr, ri, n, st);
+  } else if (hit) {
+    if (small)
+      launch_k_cast<T, uint32_t, true, false>(v, x, y, t, out, hit, rr, ri, n, st);
+    else
+      launch_k_cast<T, size_t, true, false>(v, x, y, t, out, hit, rr, ri, n, st);
+  } else {
+    if (small)
+      launch_k_cast<T, uint32_t, false, false>(v, x, y, t, out, hit, rr, ri, n, st);
+    else
+      launch_k_cast<T, size_t, false, false>(v, x, y, t, out, hit, rr, ri, n, st);
+  }
 #endif
 }
 
@@ -448,19 +475,6 @@ __global__ void k_single(CddtView c, double x, double y, double theta, int pair,
   if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
 }
 
-// One full wave: every SM holds as many 256-thread CTAs as registers allow
-// and the grid-stride loop spreads the queries evenly (no partial last wave).
-template <class T>
-static int cast_blocks(size_t n) {
-  static int per_sm = RL_GRID_PER_SM;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast<T>, 256, 0);
-    if (per_sm <= 0) per_sm = 1;
-  }
-  size_t b = (n + 255) / 256;
-  size_t cap = size_t(sm_count()) * per_sm;
-  return int(std::max<size_t>(1, std::min(b, cap)));
-}
 static int dir_blocks(size_t n) {
   size_t b = (n + 255) / 256;
   return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * 8)));

@@ -115,11 +115,61 @@ static int blocks_for(size_t work, int threads) {
   return int(std::max<size_t>(1, std::min(b, cap)));
 }
 
+int sensor_logw_launch(rl_cddt* c, const double* px, const double* py, const double* pt,
+                       size_t n, const double* scan, int nb, double fov,
+                       const rl_beam_params_t* params, const float* table, int zdim,
+                       double inv_res, double* logw, cudaStream_t st) {
+  BeamParams bp{};
+  if (params)
+    bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
+                    params->sigma_hit, params->lambda_short, params->z_max};
+  const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
+  const size_t smem = sizeof(double) * kSensorParticlesPerCta * nb;
+  if (smem > 48 * 1024)
+    RL_CK(cudaFuncSetAttribute(k_sensor_logw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  k_sensor_logw<<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp, table,
+                                         zdim, inv_res, logw);
+  RL_CK(cudaGetLastError());
+  return RL_OK;
+}
+
+static int check_sensor_args(const rl_cddt* c, const double* px, const double* py,
+                             const double* pt, size_t n, const double* scan, int32_t nbeams,
+                             const rl_beam_params_t* params, const float* table, int32_t zdim,
+                             double inv_res) {
+  if (!c || nbeams <= 0 || (n && (!px || !py || !pt || !scan))) {
+    set_error("scan length does not match beam count");  // mcl.cpp:61-62
+    return RL_EINVAL;
+  }
+  if (!table && (!params || !(params->z_max > 0.0))) {
+    set_error("beam model z_max must be positive");  // mcl.cpp:13
+    return RL_EINVAL;
+  }
+  if (table && (zdim <= 0 || !(inv_res > 0.0))) {
+    set_error("likelihood table needs zdim > 0 and inv_res > 0");
+    return RL_EINVAL;
+  }
+  return RL_OK;
+}
+
 }  // namespace rl
 
 using namespace rl;
 
 extern "C" {
+
+int rl_sensor_logw(rl_cddt* c, const double* px, const double* py, const double* pt, size_t n,
+                   const double* scan, int32_t nbeams, double fov, const rl_beam_params_t* params,
+                   const float* table, int32_t zdim, double inv_res, double* logw, void* stream) {
+  RL_TRY(check_sensor_args(c, px, py, pt, n, scan, nbeams, params, table, zdim, inv_res));
+  if (!logw && n) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  RL_TRY(sensor_logw_launch(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
+                            logw, pick_stream(c, stream)));
+  return finish(c, stream);
+}
 
 double rl_beam_likelihood(const rl_beam_params_t* p, double expected, double measured) {
   // host restatement of beam_likelihood (mcl.cpp:11-40) for table building
@@ -165,15 +215,7 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
                      const double* scan, int32_t nbeams, double fov,
                      const rl_beam_params_t* params, const float* table, int32_t zdim,
                      double inv_res, double* logw, double* weight, void* stream) {
-  if (!c || nbeams <= 0 || (n && (!px || !py || !pt || !scan))) {
-    set_error("scan length does not match beam count");  // mcl.cpp:61-62
-    return RL_EINVAL;
-  }
-  if (!table && (!params || !(params->z_max > 0.0))) {
-    set_error("beam model z_max must be positive");
-    return RL_EINVAL;
-  }
-  if (table && (zdim <= 0 || !(inv_res > 0.0))) return RL_EINVAL;
+  RL_TRY(check_sensor_args(c, px, py, pt, n, scan, nbeams, params, table, zdim, inv_res));
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
@@ -191,18 +233,8 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   double* d_sum = d_max + 1;
   int* d_flag = reinterpret_cast<int*>(d_max + 2);
   void* d_tmp = base + 16 * n + 64;
-  BeamParams bp{};
-  if (params)
-    bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
-                    params->sigma_hit, params->lambda_short, params->z_max};
-  const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
-  const size_t smem = sizeof(double) * kSensorParticlesPerCta * nbeams;
-  if (smem > 48 * 1024)
-    RL_CK(cudaFuncSetAttribute(k_sensor_logw, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  k_sensor_logw<<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nbeams, fov, bp, table,
-                                         zdim, inv_res, d_logw);
-  RL_CK(cudaGetLastError());
+  RL_TRY(sensor_logw_launch(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
+                            d_logw, st));
   RL_CK(cub::DeviceReduce::Max(d_tmp, cub_bytes, d_logw, d_max, int(n), st));
   k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(d_logw, d_max, d_w, n);
   RL_CK(cub::DeviceReduce::Sum(d_tmp, cub_bytes, d_w, d_sum, int(n), st));

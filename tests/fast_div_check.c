@@ -65,6 +65,18 @@ int main(int argc, char **argv) {
       }
     }
   }
+  /* direction_index: RN(theta * K / 2pi) with theta a float-widened angle in [0, 2pi) */
+  for (unsigned ki = 0; ki < sizeof ks / sizeof ks[0]; ki++) {
+    int K = ks[ki];
+    for (long j = 0; j < per * 64; j++) {
+      float th = (float)(u01() * TWO_PI);
+      if ((double)th >= TWO_PI) continue;
+      check((double)th * (double)K, TWO_PI);
+      double thd = u01() * TWO_PI; /* f64 angles (sensor model beams) */
+      check(thd * (double)K, TWO_PI);
+    }
+    for (int i = 0; i <= K; i++) check((double)i * TWO_PI / (double)K * (double)K, TWO_PI);
+  }
   printf("checked %ld mismatches %ld\n", checked, bad);
   return bad != 0;
 }
