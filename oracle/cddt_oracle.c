@@ -813,3 +813,94 @@ int orc_sensor_update(const orc_cddt *c, const double *px, const double *py, con
   for (long i = 0; i < n; i++) weight[i] /= sum;
   return 0;
 }
+
+/* ---- particle filter (Mcl::step, proj/src/mcl.cpp:42-56, 108-142, 176-201)
+ * with the counter-based noise of the GPU path: Philox4x32-10 keyed by the
+ * seed, counter (particle index, draw, iteration), Box-Muller normals. ---- */
+static void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; r++) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+static void philox_u2(uint64_t seed, uint32_t i, uint32_t draw, uint64_t iter, double *u0,
+                      double *u1) {
+  uint32_t c[4] = {i, draw, (uint32_t)iter, (uint32_t)(iter >> 32)};
+  philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint64_t a = ((uint64_t)c[1] << 32) | c[0], b = ((uint64_t)c[3] << 32) | c[2];
+  *u0 = (double)(a >> 11) * 0x1.0p-53;
+  *u1 = (double)(b >> 11) * 0x1.0p-53;
+}
+void orc_philox(uint32_t *c4, uint32_t k0, uint32_t k1) { philox(c4, k0, k1); }
+
+/* motion_update (mcl.cpp:42-56); noise = {a, b, c, d} of MotionNoise */
+void orc_motion_update(double *x, double *y, double *t, long n, uint64_t off, double dx,
+                       double dy, double dth, const double *noise, uint64_t seed, uint64_t iter) {
+  const double trans = hypot(dx, dy);
+  double st = noise[0] * trans + noise[1] * fabs(dth);
+  double sr = noise[2] * fabs(dth) + noise[3] * trans;
+  if (st < 1e-12) st = 1e-12;
+  if (sr < 1e-12) sr = 1e-12;
+  for (long i = 0; i < n; i++) {
+    uint32_t gi = (uint32_t)(off + (uint64_t)i);
+    double a0, a1, b0, b1;
+    philox_u2(seed, gi, 0, iter, &a0, &a1);
+    philox_u2(seed, gi, 1, iter, &b0, &b1);
+    double ra = sqrt(-2.0 * log(1.0 - a0)), rb = sqrt(-2.0 * log(1.0 - b0));
+    double n0 = ra * cos(K_TWO_PI * a1), n1 = ra * sin(K_TWO_PI * a1), n2 = rb * cos(K_TWO_PI * b1);
+    double rdx = dx + st * n0, rdy = dy + st * n1, rdt = dth + sr * n2;
+    double c = cos(t[i]), s = sin(t[i]);
+    x[i] += rdx * c - rdy * s;
+    y[i] += rdx * s + rdy * c;
+    t[i] = orc_normalize_angle_2pi(t[i] + rdt);
+  }
+}
+
+/* resample_low_variance (mcl.cpp:122-142), sequential comb; r from Philox */
+void orc_resample(const double *x, const double *y, const double *t, const double *w, long n,
+                  double *ox, double *oy, double *ot, double *ow, int64_t *src, uint64_t seed,
+                  uint64_t iter) {
+  if (n <= 0) return;
+  double u, unused;
+  philox_u2(seed, 0xFFFFFFFFu, 0xFFFFFFFFu, iter, &u, &unused);
+  const double r = (1.0 / (double)n) * u;
+  double c = w[0];
+  long i = 0;
+  for (long m = 0; m < n; m++) {
+    double target = r + (double)m / (double)n;
+    while (c < target && i + 1 < n) {
+      i++;
+      c += w[i];
+    }
+    ox[m] = x[i];
+    oy[m] = y[i];
+    ot[m] = t[i];
+    ow[m] = 1.0 / (double)n;
+    if (src) src[m] = i;
+  }
+}
+
+/* Mcl::estimate (mcl.cpp:176-187) */
+void orc_estimate(const double *x, const double *y, const double *t, const double *w, long n,
+                  double *est) {
+  double sx = 0, sy = 0, sc = 0, ss = 0, sw = 0;
+  for (long i = 0; i < n; i++) {
+    sx += w[i] * x[i];
+    sy += w[i] * y[i];
+    sc += w[i] * cos(t[i]);
+    ss += w[i] * sin(t[i]);
+    sw += w[i];
+  }
+  if (!(sw > 0.0)) sw = 1.0;
+  est[0] = sx / sw;
+  est[1] = sy / sw;
+  est[2] = orc_normalize_angle_2pi(atan2(ss, sc));
+}

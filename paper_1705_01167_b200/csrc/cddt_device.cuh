@@ -40,12 +40,15 @@ struct CddtView {
   const uint8_t* __restrict__ flags;      // w*h (build / update bookkeeping)
   const ulonglong2* __restrict__ tiles;   // tw*th occupancy + clear tiles
   int tw;
+  const uint2* __restrict__ rowbits;      // h*wpr {occupied, clear} bits, 32 cells per word
+  int wpr;
   const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
   const float* __restrict__ zp;           // zero points, ascending per row
   const SliceParam* __restrict__ slices;  // S
   const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
   int w, h, K, S;
   double max_range;
+  size_t zp_bytes;
 };
 
 __host__ __device__ __forceinline__ double fmin_std(double a, double b) { return (b < a) ? b : a; }
@@ -84,13 +87,18 @@ __device__ __forceinline__ int bit_of(int x, int y) { return ((y & 7) << 3) | (x
 #ifndef RL_TILES
 #define RL_TILES 0
 #endif
+#ifndef RL_ROWBITS
+#define RL_ROWBITS 1
+#endif
 
 // Register-resident copy of the last occupancy tile touched by a query.
 struct OccCache {
   int tile = -1;
   unsigned long long word = 0;
   __device__ __forceinline__ bool occ(const CddtView& c, int x, int y) {
-#if !RL_TILES
+#if RL_ROWBITS
+    return (__ldg(&c.rowbits[y * c.wpr + (x >> 5)].x) >> (x & 31)) & 1u;
+#elif !RL_TILES
     return (__ldg(c.flags + (size_t)y * c.w + x) & kOcc) != 0;
 #endif
     const int t = tile_of(c, x, y);
@@ -261,7 +269,14 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) return c.max_range;
   OccCache oc;
-#if RL_TILES
+#if RL_ROWBITS
+  const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
+  if ((w0.x >> (cxi & 31)) & 1u) {
+    o.hit = cyi * c.w + cxi;
+    return 0.0;
+  }
+  const bool clear0 = (w0.y >> (cxi & 31)) & 1u;
+#elif RL_TILES
   oc.tile = tile_of(c, cxi, cyi);
   const ulonglong2 t0 = __ldg(c.tiles + oc.tile);
   oc.word = t0.x;

@@ -164,7 +164,28 @@ __global__ void k_tiles(const uint8_t* __restrict__ flags, int w, int h, int tw,
   }
 }
 
+__global__ void k_rowbits(const uint8_t* __restrict__ flags, int w, int h, int wpr,
+                          uint2* __restrict__ bits) {
+  const int n = wpr * h;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int y = t / wpr, x0 = (t % wpr) * 32;
+    unsigned occ = 0, clr = 0;
+    for (int b = 0; b < 32 && x0 + b < w; b++) {
+      const uint8_t f = flags[size_t(y) * w + x0 + b];
+      if (f & kOcc) occ |= 1u << b;
+      if (f & kClear) clr |= 1u << b;
+    }
+    bits[t] = make_uint2(occ, clr);
+  }
+}
+
 int refresh_tiles(rl_cddt* c) {
+  c->wpr = (c->w + 31) / 32;
+  const size_t nw = size_t(c->wpr) * c->h;
+  if (c->rowbits.n != nw) RL_TRY(c->rowbits.alloc(nw));
+  k_rowbits<<<int(std::min<size_t>((nw + 255) / 256, size_t(sm_count()) * 16)), 256, 0,
+              c->stream>>>(c->flags.p, c->w, c->h, c->wpr, c->rowbits.p);
+  RL_CK(cudaGetLastError());
   c->tw = (c->w + 7) / 8;
   c->th = (c->h + 7) / 8;
   const size_t n = size_t(c->tw) * c->th;
@@ -341,6 +362,9 @@ int build_structure(rl_cddt* c) {
 
 // ---------------------------------------------------------------------------
 // K3: batched casts, one thread per query, grid-stride.
+#ifndef RL_L2_PERSIST
+#define RL_L2_PERSIST 0
+#endif
 #ifndef RL_STREAM_IO
 #define RL_STREAM_IO 1
 #endif
@@ -393,7 +417,35 @@ static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t,
     if (per_sm <= 0) per_sm = 1;
   }
   const size_t b = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * per_sm));
+#if RL_L2_PERSIST
+  // keep the zero points L2-resident against the streaming query traffic
+  static size_t persist_max = 0;
+  if (!persist_max) {
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    persist_max = size_t(mx > 0 ? mx : 1);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_max);
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  const size_t zb = v.zp_bytes;
+  attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(v.zp);
+  attr[0].val.accessPolicyWindow.num_bytes = zb;
+  attr[0].val.accessPolicyWindow.hitRatio =
+      zb > persist_max ? float(double(persist_max) / double(zb)) : 1.0f;
+  attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(b));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_cast<T, I, HIT, RES>, v, x, y, t, out, hit, rr, ri, I(n));
+#else
   k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
+#endif
 }
 
 #ifndef RL_CAST_SM
@@ -652,6 +704,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     c->flags.release();
     c->tiles.release();
+    c->rowbits.release();
     c->row_off.release();
     c->zp.release();
     c->d_slices.release();

@@ -113,6 +113,8 @@ struct rl_cddt {
   rl::DevBuf<uint8_t> flags;        // w*h
   rl::DevBuf<ulonglong2> tiles;     // 8x8 occupancy/clear tiles for queries
   int tw = 0, th = 0;
+  rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
+  int wpr = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
   rl::DevBuf<float> zp;             // capacity >= zero_points
   rl::DevBuf<rl::SliceParam> d_slices;
@@ -125,6 +127,8 @@ struct rl_cddt {
     v.flags = flags.p;
     v.tiles = tiles.p;
     v.tw = tw;
+    v.rowbits = rowbits.p;
+    v.wpr = wpr;
     v.row_off = row_off.p;
     v.zp = zp.p;
     v.slices = d_slices.p;
@@ -134,6 +138,7 @@ struct rl_cddt {
     v.K = K;
     v.S = S;
     v.max_range = max_range;
+    v.zp_bytes = size_t(zero_points) * sizeof(float);
     return v;
   }
 };

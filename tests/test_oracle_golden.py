@@ -205,3 +205,18 @@ def test_oracle_sensor_matches_reference(oracle_mod, synth):
     for e, m in [(0.0, 0.0), (10.0, 12.5), (199.5, 200.0), (-3.0, 250.0)]:
         assert oracle_mod.orc_lib().orc_beam_likelihood(p.ctypes.data, e, m) == \
             oracle_mod.ref_lib().ref_beam_likelihood(p.ctypes.data, e, m)
+
+
+def test_philox_known_answer(oracle_mod):
+    import ctypes as C
+    # Philox4x32-10 known-answer vectors (Random123 kat_vectors)
+    L = oracle_mod.orc_lib()
+    L.orc_philox.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32]
+    c = np.zeros(4, np.uint32)
+    L.orc_philox(c.ctypes.data, 0, 0)
+    assert [hex(v) for v in c] == ["0x6627e8d5", "0xe169c58d", "0xbc57ac4c", "0x9b00dbd8"]
+    c = np.full(4, 0xFFFFFFFF, np.uint32)
+    L.orc_philox(c.ctypes.data, 0xFFFFFFFF, 0xFFFFFFFF)
+    assert [hex(v) for v in c] == ["0x408f276d", "0x41c83b0e", "0xa20bc7c6", "0x6d5451fd"]
+
+
