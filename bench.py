@@ -158,6 +158,50 @@ def reference_cpu(g, qx, qy, qt, sample: int, snapshot: bytes | None, threads: i
     return ref, r["out64"], dt, setup, how
 
 
+def pf_update_timing(iterations: int, device: int):
+    """BASELINE config 4: full particle-filter update (motion, fused CDDT sensor
+    model with the 501x501 table, normalisation, estimate, low-variance
+    resampling) for 40,000 particles x 61 beams on the 2000x2000 maze,
+    theta_disc 120, max_range 500, along a seeded 1 px/step trajectory."""
+    import numpy as np
+    import torch
+
+    import paper_1705_01167_b200 as rl
+    from paper_1705_01167_b200 import mcl, synth
+    g = synth.maze_map()
+    x, y, t = synth.free_pose(g, 15, seed=8)
+    pose, odo = synth.trajectory(g, x, y, t, iterations, 1.0, 15.0, seed=4)
+    grid = rl.OccupancyGrid.from_array(g)
+    method = rl.make_method("cddt", grid, rl.RangeMethodConfig(500.0, 120), device=device)
+    beam = rl.BeamModelParams(sigma_hit=8.0, z_max=500.0)
+    table = torch.from_numpy(rl.beam_table(beam, 501, 1.0)).cuda(device)
+    cfg = mcl.MclConfig(particle_count=40_000, beam=beam, seed=5,
+                        motion=mcl.MotionNoise(1.0, 0.0, 0.0, 0.02))  # sigma_xy 1 px, sigma_th 0.02
+    f = mcl.Mcl(method, cfg, table=table)
+    f.init_gaussian(x, y, t, 10.0, 0.1)
+    scans = [torch.from_numpy(synth.scan(g, *pose[k + 1], 61, 4.71238898038469, 500.0, 8.0, 0.05,
+                                         seed=1000 + k)).cuda(device) for k in range(iterations)]
+    for k in range(5):
+        f.step(*odo[k], scans[k])
+    torch.cuda.synchronize()
+    times, errs = [], []
+    for k in range(iterations):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = f.step(*odo[k], scans[k])
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        errs.append(float(np.hypot(r.estimate.x - pose[k + 1][0], r.estimate.y - pose[k + 1][1])))
+    times = np.array(times)
+    return {"workload": "BASELINE config 4: 40,000 particles x 61 beams, 2000x2000 maze, "
+                        "theta_disc=120, 501x501 table, 1 GPU",
+            "iterations": iterations, "ms_per_update_p50": float(np.median(times)),
+            "ms_per_update_mean": float(times.mean()), "ms_per_update_p99":
+            float(np.percentile(times, 99)), "casts_per_update": 40_000 * 61,
+            "median_position_error_px": float(np.median(errs[10:]))}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -275,6 +319,8 @@ def run_ours(args, rank, world, local_rank):
                              "parity_mismatches": mism},
             "clocks": clk.summary(),
         }
+        if args.pf_iterations > 0:
+            line["pf_update"] = pf_update_timing(args.pf_iterations, local_rank)
     return line
 
 
@@ -322,6 +368,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=16_000_000)
     ap.add_argument("--sector-sample", type=int, default=200_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--pf-iterations", type=int, default=1000)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
