@@ -32,6 +32,8 @@ def build(ref: bool = True) -> None:
     targets = ["all"]
     if ref and (REF_ROOT / "src" / "cddt.cpp").exists():
         targets.append("ref")
+        if (HERE.parent / "paper_1705_01167_b200" / "librl_cddt.so").exists():
+            targets.append("dropin")
     subprocess.run(["make", "-s", "-C", str(HERE), *targets], check=True)
 
 

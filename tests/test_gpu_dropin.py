@@ -1,0 +1,22 @@
+"""GPU: the reference's own code (Cddt, sensor_update, Mcl; compiled unmodified
+into oracle/_ref/dropin_check) driven with the GPU RangeMethod adapter
+(include/rl_cddt_rangemethod.hpp) gives bit-identical casts, weights and
+closed-loop estimates to the reference's CPU CDDT."""
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+EXE = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "dropin_check"
+
+
+def test_reference_code_with_gpu_method(rl, oracle_mod):
+    if not EXE.exists():
+        pytest.skip("oracle/_ref/dropin_check not built (needs the reference sources)")
+    r = subprocess.run([str(EXE)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("DROPIN")]
+    assert len(lines) == 4, r.stdout + r.stderr
+    assert r.returncode == 0 and all(" PASS " in ln for ln in lines), r.stdout + r.stderr
