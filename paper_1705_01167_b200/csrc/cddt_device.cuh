@@ -269,6 +269,20 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) return c.max_range;
   OccCache oc;
+  // Issue the independent gathers of this query together: the origin cell's
+  // bits and the row offsets do not depend on each other, so the row offsets
+  // are requested before the origin test resolves (they are simply unused when
+  // the origin is occupied).
+  const bool forward = a < c.S;
+  const int s = forward ? a : a - c.S;
+  const SliceParam sp = c.slices[s];
+  const double xq = x * sp.cos_t + y * sp.sin_t;                 // cddt.hpp:31
+  const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;  // cddt.hpp:32
+  int row = (int)yq;
+  if (row < 0) row = 0;
+  if (row >= sp.bin_count) row = sp.bin_count - 1;
+  const uint32_t g = sp.row_base + (uint32_t)row;
+  const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
 #if RL_ROWBITS
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {
@@ -294,14 +308,6 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   }
   const bool clear0 = (f0 & kClear) != 0;
 #endif
-  const bool forward = a < c.S;
-  const int s = forward ? a : a - c.S;
-  const SliceParam sp = c.slices[s];
-  const double xq = x * sp.cos_t + y * sp.sin_t;                 // cddt.hpp:31
-  const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;  // cddt.hpp:32
-  int row = (int)yq;
-  if (row < 0) row = 0;
-  if (row >= sp.bin_count) row = sp.bin_count - 1;
   const double4 dir = c.dirs[a];
   const double dx = dir.x, dy = dir.y;
 
@@ -320,8 +326,6 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
 
   double result = c.max_range;
   const double gw = (double)c.w, gh = (double)c.h;
-  const uint32_t g = sp.row_base + (uint32_t)row;
-  const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
   const float* __restrict__ v = c.zp + lo;
   // std::upper_bound (forward, xq < double(v)) / std::lower_bound (backward,
   // double(v) < xq): the partition point of a monotone predicate over the
@@ -364,6 +368,69 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     break;
   }
   return result;
+}
+
+}  // namespace rl
+
+namespace rl {
+
+// First phase of directional_cast for the two-phase batch kernel: everything
+// up to and including the first candidate's landing-cell probe, with no
+// RayWalker. Returns true with *result set when the query is settled there
+// (off-map or occupied origin, no candidate, candidate beyond max_range, or
+// an interior landing hit) — exactly where cddt.cpp:207-269 would return —
+// and false when the exact answer needs the walker (a non-clear origin's
+// near field, or a candidate whose landing probe does not settle it); the
+// caller then runs the full directional_cast for that query.
+__device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double x, double y,
+                                                      int a, double* result) {
+  const int cxi = (int)floor(x), cyi = (int)floor(y);
+  if (!in_bounds(c, cxi, cyi)) {
+    *result = c.max_range;
+    return true;
+  }
+  const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
+  if ((w0.x >> (cxi & 31)) & 1u) {
+    *result = 0.0;
+    return true;
+  }
+  if (!((w0.y >> (cxi & 31)) & 1u)) return false;  // near field needs the walker
+  const bool forward = a < c.S;
+  const int s = forward ? a : a - c.S;
+  const SliceParam sp = c.slices[s];
+  const double xq = x * sp.cos_t + y * sp.sin_t;
+  const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;
+  int row = (int)yq;
+  if (row < 0) row = 0;
+  if (row >= sp.bin_count) row = sp.bin_count - 1;
+  const uint32_t g = sp.row_base + (uint32_t)row;
+  const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
+  const uint32_t first = partition_point(c.zp + lo, hi - lo, xq, forward);
+  const int n = (int)(hi - lo);
+  const int idx = forward ? (int)first : (int)first - 1;
+  if (idx < 0 || idx >= n) {
+    *result = c.max_range;
+    return true;
+  }
+  const double vv = (double)__ldg(c.zp + lo + idx);
+  const double d = forward ? vv - xq : xq - vv;
+  if (d >= c.max_range) {
+    *result = c.max_range;
+    return true;
+  }
+  const double4 dir = c.dirs[a];
+  const double px = x + d * dir.x, py = y + d * dir.y;
+  if (px >= 0.0 && py >= 0.0 && px < (double)c.w && py < (double)c.h) {
+    const int hx = (int)px, hy = (int)py;
+    const double fx = px - (double)hx, fy = py - (double)hy;
+    if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
+        fy < 1.0 - kLatticeEps &&
+        ((__ldg(&c.rowbits[hy * c.wpr + (hx >> 5)].x) >> (hx & 31)) & 1u)) {
+      *result = d;
+      return true;
+    }
+  }
+  return false;
 }
 
 }  // namespace rl

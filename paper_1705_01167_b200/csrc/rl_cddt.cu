@@ -365,6 +365,9 @@ int build_structure(rl_cddt* c) {
 #ifndef RL_L2_PERSIST
 #define RL_L2_PERSIST 0
 #endif
+#ifndef RL_PREFETCH
+#define RL_PREFETCH 0
+#endif
 #ifndef RL_STREAM_IO
 #define RL_STREAM_IO 1
 #endif
@@ -380,15 +383,31 @@ __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T*
                                               T* __restrict__ out, int32_t* __restrict__ hit,
                                               int64_t* __restrict__ res_row,
                                               int32_t* __restrict__ res_idx, I n) {
-  for (I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); i < n;
-       i += I(gridDim.x) * I(blockDim.x)) {
-#if RL_STREAM_IO
+  const I stride = I(gridDim.x) * I(blockDim.x);
+  I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x);
+#if RL_PREFETCH
+  // software pipeline: the next query's inputs are requested while the
+  // current one walks its dependent gathers, hiding the DRAM stream latency
+  T nx = T(0), ny = T(0), nt = T(0);
+  if (i < n) {
+    nx = __ldcs(qx + i);
+    ny = __ldcs(qy + i);
+    nt = __ldcs(qt + i);
+  }
+#endif
+  for (; i < n; i += stride) {
+#if RL_PREFETCH
+    const double x = double(nx), y = double(ny);
+    const double th = normalize_angle_2pi(double(nt));  // RayQuery ctor, raycast.hpp:47
+    if (i + stride < n) {
+      nx = __ldcs(qx + i + stride);
+      ny = __ldcs(qy + i + stride);
+      nt = __ldcs(qt + i + stride);
+    }
+#else
     // query streams are touched once: evict-first so the structure stays in L2
     const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
     const double th = normalize_angle_2pi(double(__ldcs(qt + i)));  // RayQuery ctor, raycast.hpp:47
-#else
-    const double x = double(qx[i]), y = double(qy[i]);
-    const double th = normalize_angle_2pi(double(qt[i]));
 #endif
     const int a = direction_index(th, c.K);
     CastOut o;
@@ -403,6 +422,64 @@ __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T*
       if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
       if (res_idx) res_idx[i] = o.res_idx;
     }
+  }
+}
+
+#ifndef RL_TWO_PHASE
+#define RL_TWO_PHASE 0
+#endif
+// Two-phase batch: phase 1 settles every query that needs no RayWalker with
+// straight-line code (high SIMT efficiency) and appends the rest as compact
+// (x, y, theta, index) records; phase 2 runs the full directional_cast over
+// those records only, so the divergent walker code runs with lanes that all
+// need it.
+struct DeferredQuery {
+  float x, y, t;
+  uint32_t i;
+};
+
+template <class T>
+__global__ void __launch_bounds__(256) k_cast_p1(CddtView c, const T* __restrict__ qx,
+                                                 const T* __restrict__ qy,
+                                                 const T* __restrict__ qt, T* __restrict__ out,
+                                                 uint32_t n, DeferredQuery* __restrict__ q,
+                                                 unsigned* __restrict__ qn) {
+  const unsigned lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    bool defer = false;
+    float fx = 0, fy = 0, ft = 0;
+    if (i < n) {
+      fx = __ldcs(qx + i);
+      fy = __ldcs(qy + i);
+      ft = __ldcs(qt + i);
+      const double th = normalize_angle_2pi(double(ft));
+      double r;
+      if (directional_cast_fast(c, double(fx), double(fy), direction_index(th, c.K), &r))
+        __stcs(out + i, T(r));
+      else
+        defer = true;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, defer);
+    unsigned pos0 = 0;
+    if (lane == 0 && ballot) pos0 = atomicAdd(qn, __popc(ballot));
+    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+    if (defer) q[pos0 + __popc(ballot & ((1u << lane) - 1))] = DeferredQuery{fx, fy, ft, i};
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast_p2(CddtView c,
+                                                               const DeferredQuery* __restrict__ q,
+                                                               const unsigned* __restrict__ qn,
+                                                               T* __restrict__ out) {
+  const unsigned m = *qn;
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    const DeferredQuery d = q[k];
+    const double th = normalize_angle_2pi(double(d.t));
+    CastOut o;
+    const double r = directional_cast(c, double(d.x), double(d.y), direction_index(th, c.K), o);
+    __stcs(out + d.i, T(r));
   }
 }
 
@@ -492,6 +569,27 @@ static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T*
 #else
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
+#if RL_TWO_PHASE
+  if (!rr && !ri && !hit && small) {
+    rl_cddt* cm = const_cast<rl_cddt*>(c);
+    const size_t need = sizeof(DeferredQuery) * n + 256;
+    if (cm->defer_ws.n < need) cm->defer_ws.alloc(need);
+    unsigned* qn = reinterpret_cast<unsigned*>(cm->defer_ws.p);
+    DeferredQuery* q = reinterpret_cast<DeferredQuery*>(cm->defer_ws.p + 256);
+    cudaMemsetAsync(qn, 0, sizeof(unsigned), st);
+    static int p1 = 0, p2 = 0;
+    if (!p1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_cast_p1<T>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_cast_p2<T>, 256, 0);
+      p1 = std::max(p1, 1);
+      p2 = std::max(p2, 1);
+    }
+    const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
+    k_cast_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
+    k_cast_p2<T><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, out);
+    return;
+  }
+#endif
   if (rr || ri) {
     launch_k_cast<T, size_t, true, true>(v, x, y, t, out, hit, rr, ri, n, st);
   } else if (hit) {
@@ -711,6 +809,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->d_dirs.release();
     c->d_scalar.release();
     c->ws.release();
+    c->defer_ws.release();
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;

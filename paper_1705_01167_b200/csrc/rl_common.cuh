@@ -121,6 +121,7 @@ struct rl_cddt {
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
+  rl::DevBuf<uint8_t> defer_ws;     // two-phase cast: deferred-query records
 
   rl::CddtView view() const {
     rl::CddtView v;
