@@ -35,10 +35,11 @@ struct WalkState {
                                         double ry, double tt) {
     t = tt;  // ray_walker.hpp:62-73
     const double px = x + tt * dx, py = y + tt * dy;
-    cx = (int)floor(px);
-    cy = (int)floor(py);
-    if (dx < 0 && px == (double)cx) cx--;
-    if (dy < 0 && py == (double)cy) cy--;
+    const Floor fx = floor2(px), fy = floor2(py);
+    cx = fx.i;
+    cy = fy.i;
+    if (dx < 0 && px == fx.d) cx--;
+    if (dy < 0 && py == fy.d) cy--;
     tnx = boundary_t(dx, x, cx, rx);
     tny = boundary_t(dy, y, cy, ry);
   }

@@ -56,6 +56,40 @@ __host__ __device__ __forceinline__ double fmax_std(double a, double b) { return
 
 __device__ __forceinline__ long iround(double v) { return (long)ceil(v - 0.5); }  // raycast.hpp:17
 
+// Exact double <-> int helpers that stay off the XU (conversion) pipe, which
+// the cast kernel otherwise saturates (profiles/r01/ncu_k_cast_v3.txt):
+// floor via the 1.5*2^52 rounding constant (RN(v) lands in the low mantissa
+// bits, then one compare corrects to floor), int -> double via the 2^52 + 2^31
+// bias. Both are exact for |v| < 2^30; anything else takes the IEEE path.
+struct Floor {
+  int i;
+  double d;
+};
+#ifndef RL_NOXU_FLOOR
+#define RL_NOXU_FLOOR 0
+#endif
+#ifndef RL_NOXU_I2D
+#define RL_NOXU_I2D 0
+#endif
+__device__ __forceinline__ Floor floor2(double v) {
+  if (!RL_NOXU_FLOOR || !(fabs(v) < 1073741824.0)) {
+    const double f = floor(v);
+    return Floor{(int)f, f};
+  }
+  const double t = v + 6755399441055744.0;
+  int i = __double2loint(t);
+  double r = t - 6755399441055744.0;  // RN(v), exact
+  if (r > v) {
+    i -= 1;
+    r -= 1.0;
+  }
+  return Floor{i, r};
+}
+__device__ __forceinline__ double i2d(int v) {
+  if (!RL_NOXU_I2D) return (double)v;
+  return __hiloint2double(0x43300000, v ^ (int)0x80000000) - 4503601774854144.0;
+}
+
 __device__ __forceinline__ double normalize_angle_2pi(double t) {  // raycast.hpp:20-25
   if (t >= 0.0 && t < kTwoPi) return t;  // fmod(t, 2pi) == t exactly here
   t = fmod(t, kTwoPi);
@@ -69,12 +103,12 @@ constexpr double kInvTwoPi = 1.0 / kTwoPi;  // RN(1/2pi), folded at compile time
 
 __device__ __forceinline__ int direction_index(double theta, int K) {  // raycast.hpp:36-40
   // iround(theta * K / 2pi) % K; the quotient is the correctly rounded one
-  const double v = ceil(div_rn(theta * (double)K, kTwoPi, kInvTwoPi) - 0.5);
-  if (v >= 0.0 && v <= (double)K) {  // theta in [0, 2pi): plain range, no modulo
-    const int i = (int)v;
-    return i == K ? 0 : i;
-  }
-  long i = (long)v % K;
+  const double t = div_rn(theta * (double)K, kTwoPi, kInvTwoPi) - 0.5;
+  const Floor f = floor2(-t);  // ceil(t) = -floor(-t)
+  const int ci = -f.i;
+  if (ci >= 0 && ci <= K && fabs(t) < 1073741824.0)  // theta in [0, 2pi): no modulo
+    return ci == K ? 0 : ci;
+  long i = (long)ceil(t) % K;
   if (i < 0) i += K;
   return (int)i;
 }
@@ -135,22 +169,88 @@ __device__ __forceinline__ double div_rn(double a, double d, double r) {  // NOL
 }
 
 __device__ __forceinline__ double boundary_t(double d, double o, int cc, double r) {  // ray_walker.hpp:75-79
-  if (d > 0) return div_rn((double)cc + 1.0 - o, d, r);
-  if (d < 0) return div_rn((double)cc - o, d, r);
+  if (d > 0) return div_rn(i2d(cc) + 1.0 - o, d, r);
+  if (d < 0) return div_rn(i2d(cc) - o, d, r);
   return __longlong_as_double(0x7ff0000000000000ll);
 }
 
+#ifndef RL_WALK_BRANCHFREE
+#define RL_WALK_BRANCHFREE 0
+#endif
+
+// RayWalker (ray_walker.hpp:21-104). The per-axis sign logic of boundary_t
+// and advance() is hoisted into per-query constants (step sign, boundary
+// bias 1.0/0.0, axis-parallel flag), so a walker step is straight-line code
+// with selects: lanes walking in different directions no longer diverge.
+// Each boundary value is still ((double)c + 1.0 - o) / d or ((double)c - o)/d
+// rounded exactly as the reference computes it.
 struct Walker {
   double ox, oy, dx, dy, rx, ry, t, tnx, tny;
   int cx, cy;
+#if RL_WALK_BRANCHFREE
+  double bx, by;   // 1.0 when the axis direction is positive, else 0.0
+  int sx, sy;      // cell step along each axis
+  bool zx, zy;     // axis-parallel: boundary parameter is +inf
 
+  __device__ __forceinline__ double bnd_x(int c) const {
+    const double v = div_rn((i2d(c) + bx) - ox, dx, rx);
+    return zx ? __longlong_as_double(0x7ff0000000000000ll) : v;
+  }
+  __device__ __forceinline__ double bnd_y(int c) const {
+    const double v = div_rn((i2d(c) + by) - oy, dy, ry);
+    return zy ? __longlong_as_double(0x7ff0000000000000ll) : v;
+  }
   __device__ __forceinline__ void place(double tt) {  // ray_walker.hpp:62-73
     t = tt;
     double px = ox + tt * dx, py = oy + tt * dy;
-    cx = (int)floor(px);
-    cy = (int)floor(py);
-    if (dx < 0 && px == (double)cx) cx--;
-    if (dy < 0 && py == (double)cy) cy--;
+    const Floor fx = floor2(px), fy = floor2(py);
+    cx = fx.i - ((dx < 0 && px == fx.d) ? 1 : 0);
+    cy = fy.i - ((dy < 0 && py == fy.d) ? 1 : 0);
+    tnx = bnd_x(cx);
+    tny = bnd_y(cy);
+  }
+  __device__ __forceinline__ void init(double x, double y, const double4& dir) {
+    ox = x;
+    oy = y;
+    dx = dir.x;
+    dy = dir.y;
+    rx = dir.z;
+    ry = dir.w;
+    bx = dx > 0 ? 1.0 : 0.0;
+    by = dy > 0 ? 1.0 : 0.0;
+    sx = dx > 0 ? 1 : -1;
+    sy = dy > 0 ? 1 : -1;
+    zx = !(dx > 0) && !(dx < 0);
+    zy = !(dy > 0) && !(dy < 0);
+    place(0.0);
+  }
+  __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
+    if (tt > t) place(tt);
+  }
+  __device__ __forceinline__ void advance() {  // ray_walker.hpp:81-97
+    // equal parameters: exact corner crossing, both axes step (diagonal)
+    const bool stx = tnx <= tny, sty = tny <= tnx;
+    t = stx ? tnx : tny;
+    const int ncx = cx + sx, ncy = cy + sy;
+    const double ntx = bnd_x(ncx), nty = bnd_y(ncy);
+    if (stx) {
+      cx = ncx;
+      tnx = ntx;
+    }
+    if (sty) {
+      cy = ncy;
+      tny = nty;
+    }
+  }
+#else
+  __device__ __forceinline__ void place(double tt) {  // ray_walker.hpp:62-73
+    t = tt;
+    double px = ox + tt * dx, py = oy + tt * dy;
+    const Floor fx = floor2(px), fy = floor2(py);
+    cx = fx.i;
+    cy = fy.i;
+    if (dx < 0 && px == fx.d) cx--;
+    if (dy < 0 && py == fy.d) cy--;
     tnx = boundary_t(dx, ox, cx, rx);
     tny = boundary_t(dy, oy, cy, ry);
   }
@@ -183,6 +283,7 @@ struct Walker {
       tny = boundary_t(dy, oy, cy, ry);
     }
   }
+#endif
   __device__ __forceinline__ double scan_to(const CddtView& c, OccCache& oc, double lim) {  // :51-59
     for (;;) {
       if (!in_bounds(c, cx, cy)) return kWalkExit;
@@ -266,7 +367,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   o.hit = -1;
   o.res_idx = -1;
   o.res_g = 0;
-  const int cxi = (int)floor(x), cyi = (int)floor(y);
+  const int cxi = floor2(x).i, cyi = floor2(y).i;
   if (!in_bounds(c, cxi, cyi)) return c.max_range;
   OccCache oc;
   // Issue the independent gathers of this query together: the origin cell's
@@ -278,7 +379,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   const SliceParam sp = c.slices[s];
   const double xq = x * sp.cos_t + y * sp.sin_t;                 // cddt.hpp:31
   const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;  // cddt.hpp:32
-  int row = (int)yq;
+  int row = floor2(yq).i;  // == int(yq) after the clamp below (differs only for yq < 0)
   if (row < 0) row = 0;
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   const uint32_t g = sp.row_base + (uint32_t)row;
@@ -341,8 +442,9 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     // landing-cell probe (cddt.cpp:239-253)
     const double px = x + d * dx, py = y + d * dy;
     if (px >= 0.0 && py >= 0.0 && px < gw && py < gh) {
-      const int hx = (int)px, hy = (int)py;
-      const double fx = px - (double)hx, fy = py - (double)hy;
+      const Floor flx = floor2(px), fly = floor2(py);  // px, py >= 0: int() == floor
+      const int hx = flx.i, hy = fly.i;
+      const double fx = px - flx.d, fy = py - fly.d;
       if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
           fy < 1.0 - kLatticeEps && oc.occ(c, hx, hy)) {
         o.hit = hy * c.w + hx;
@@ -384,7 +486,7 @@ namespace rl {
 // caller then runs the full directional_cast for that query.
 __device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double x, double y,
                                                       int a, double* result) {
-  const int cxi = (int)floor(x), cyi = (int)floor(y);
+  const int cxi = floor2(x).i, cyi = floor2(y).i;
   if (!in_bounds(c, cxi, cyi)) {
     *result = c.max_range;
     return true;
@@ -400,7 +502,7 @@ __device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double 
   const SliceParam sp = c.slices[s];
   const double xq = x * sp.cos_t + y * sp.sin_t;
   const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;
-  int row = (int)yq;
+  int row = floor2(yq).i;  // == int(yq) after the clamp below (differs only for yq < 0)
   if (row < 0) row = 0;
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   const uint32_t g = sp.row_base + (uint32_t)row;
@@ -421,8 +523,9 @@ __device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double 
   const double4 dir = c.dirs[a];
   const double px = x + d * dir.x, py = y + d * dir.y;
   if (px >= 0.0 && py >= 0.0 && px < (double)c.w && py < (double)c.h) {
-    const int hx = (int)px, hy = (int)py;
-    const double fx = px - (double)hx, fy = py - (double)hy;
+    const Floor flx = floor2(px), fly = floor2(py);
+    const int hx = flx.i, hy = fly.i;
+    const double fx = px - flx.d, fy = py - fly.d;
     if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
         fy < 1.0 - kLatticeEps &&
         ((__ldg(&c.rowbits[hy * c.wpr + (hx >> 5)].x) >> (hx & 31)) & 1u)) {

@@ -27,6 +27,14 @@ else:
     g, K, mr, prune = synth.rect_map(), 108, 300.0, False
 c = rl.Cddt(rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(mr, K), prune=prune)
 qx, qy, qt = synth.free_queries(g, n, seed=7)
+if os.environ.get("SORT") == "theta":  # locality experiment: queries ordered by direction
+    o = np.argsort(qt, kind="stable")
+    qx, qy, qt = qx[o], qy[o], qt[o]
+elif os.environ.get("SORT") == "chunk":  # ordered by direction within 8M-query chunks
+    ch = 8_000_000
+    for s0 in range(0, n, ch):
+        o = np.argsort(qt[s0:s0 + ch], kind="stable") + s0
+        qx[s0:s0 + ch], qy[s0:s0 + ch], qt[s0:s0 + ch] = qx[o], qy[o], qt[o]
 dx, dy, dt = (torch.from_numpy(a).cuda() for a in (qx, qy, qt))
 out = torch.empty_like(dx)
 for _ in range(3):
