@@ -202,6 +202,76 @@ def pf_update_timing(iterations: int, device: int):
             "median_position_error_px": float(np.median(errs[10:]))}
 
 
+def other_configs(device: int, rounds: int = 20):
+    """BASELINE configs 1, 2 and 5 on one GPU (timings only; parity for each
+    is in tests/test_gpu_*.py)."""
+    import numpy as np
+    import torch
+
+    import paper_1705_01167_b200 as rl
+    from paper_1705_01167_b200 import synth
+    out = {}
+
+    def ev_time(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    # config 1: 500x500 rectangles, theta_disc 108, max_range 300, 100k queries
+    g = synth.rect_map()
+    t0 = time.perf_counter()
+    c = rl.Cddt(rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(300.0, 108), device=device)
+    build = time.perf_counter() - t0
+    qx, qy, qt = (torch.from_numpy(a).cuda(device) for a in synth.free_queries(g, 100_000, seed=7))
+    o = torch.empty_like(qx)
+    ms = ev_time(lambda: c.cast_batch(qx, qy, qt, out=o), 200)
+    out["config1"] = {"workload": "500x500 rects, theta_disc=108, max_range=300, CDDT, 100k queries",
+                      "build_s": build, "zero_points": c.zero_point_count(),
+                      "ms_per_100k_batch": ms, "casts_per_s": 100_000 / ms * 1e3}
+    # config 2: sensor model, 2500 particles x 61 beams, 501x501 table
+    g2 = synth.maze_map()
+    m2 = rl.make_method("cddt", rl.OccupancyGrid.from_array(g2), rl.RangeMethodConfig(500.0, 120),
+                        device=device)
+    x, y, t = synth.free_pose(g2, 10, seed=5)
+    px, py, pt = synth.particles(x, y, t, 2500, 10.0, 0.1, seed=9)
+    scan = torch.from_numpy(synth.scan(g2, x, y, t, 61, 4.71238898038469, 500.0, 8.0, 0.05,
+                                       seed=13)).cuda(device)
+    beam = rl.BeamModelParams(sigma_hit=8.0, z_max=500.0)
+    table = torch.from_numpy(rl.beam_table(beam, 501, 1.0)).cuda(device)
+    parts = {k: torch.from_numpy(v).cuda(device) for k, v in
+             dict(x=px, y=py, theta=pt, weight=np.zeros_like(px)).items()}
+    spec = rl.ScanSpec(61, 4.71238898038469)
+    ms2 = ev_time(lambda: rl.sensor_update(parts, m2, scan, spec, beam, table=table), 200)
+    out["config2"] = {"workload": "2000x2000 maze, theta_disc=120, max_range=500, 2500 particles x "
+                                  "61 beams, 501x501 table", "ms_per_sensor_update": ms2,
+                      "casts_per_s": 2500 * 61 / ms2 * 1e3}
+    # config 5: 2000x2000 maze, theta_disc 108; rounds of 50 random 3x3 edits + 1M queries
+    c5 = rl.Cddt(rl.OccupancyGrid.from_array(g2), rl.RangeMethodConfig(0.0, 108), device=device)
+    q5 = [torch.from_numpy(a).cuda(device) for a in synth.free_queries(g2, 1_000_000, seed=31)]
+    o5 = torch.empty_like(q5[0])
+    upd, qry = [], []
+    for r in range(rounds):
+        xy, occ = synth.block_edits(2000, 2000, 50, seed=9000 + r)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        c5.set_occupancy_batch(xy, occ)
+        upd.append(time.perf_counter() - t0)
+        qry.append(ev_time(lambda: c5.cast_batch(*q5, out=o5), 3))
+    out["config5"] = {"workload": "2000x2000 maze, theta_disc=108, rounds of 50 random 3x3 "
+                                  "insert/remove blocks + 1M queries", "rounds": rounds,
+                      "ms_per_update_round_p50": 1e3 * float(np.median(upd)),
+                      "ms_per_1M_queries_p50": float(np.median(qry)),
+                      "zero_points_after": c5.zero_point_count()}
+    return out
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -219,6 +289,7 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_1705_01167_b200 as rl
 
+    local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     n = args.queries
     g, qx, qy, qt, np = make_workload(n, rank)
@@ -259,8 +330,9 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         barrier()
         t_e2e = e0.elapsed_time(e1) / 1e3
-    if world > 1:
-        tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:  # max over ranks
+        tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64,
+                          device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev, t_e2e = tt.tolist()
     if not torch.equal(out.cpu(), host_out):
@@ -321,6 +393,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if args.pf_iterations > 0:
             line["pf_update"] = pf_update_timing(args.pf_iterations, local_rank)
+        if not args.no_extra:
+            line["other_configs"] = other_configs(local_rank)
     return line
 
 
@@ -369,6 +443,7 @@ def main():
     ap.add_argument("--sector-sample", type=int, default=200_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     ap.add_argument("--pf-iterations", type=int, default=1000)
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 1/2/5 timings")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -381,8 +456,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: host-logic checks only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(line), flush=True)
