@@ -44,6 +44,7 @@ struct CddtView {
   int wpr;
   const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
   const float* __restrict__ zp;           // zero points, ascending per row
+  const float* __restrict__ zs;           // zs[j] = zp[16 j]: a search guide over the CSR
   const SliceParam* __restrict__ slices;  // S
   const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
   int w, h, K, S;
@@ -175,7 +176,7 @@ __device__ __forceinline__ double boundary_t(double d, double o, int cc, double 
 }
 
 #ifndef RL_WALK_BRANCHFREE
-#define RL_WALK_BRANCHFREE 0
+#define RL_WALK_BRANCHFREE 1
 #endif
 
 // RayWalker (ray_walker.hpp:21-104). The per-axis sign logic of boundary_t
@@ -224,6 +225,24 @@ struct Walker {
     zy = !(dy > 0) && !(dy < 0);
     place(0.0);
   }
+  // emplace + seek(tt): place() resets the whole state, so one place at max(0, tt)
+  __device__ __forceinline__ void init_at(double x, double y, const double4& dir, double tt) {
+    ox = x;
+    oy = y;
+    dx = dir.x;
+    dy = dir.y;
+    rx = dir.z;
+    ry = dir.w;
+#if RL_WALK_BRANCHFREE
+    bx = dx > 0 ? 1.0 : 0.0;
+    by = dy > 0 ? 1.0 : 0.0;
+    sx = dx > 0 ? 1 : -1;
+    sy = dy > 0 ? 1 : -1;
+    zx = !(dx > 0) && !(dx < 0);
+    zy = !(dy > 0) && !(dy < 0);
+#endif
+    place(tt > 0.0 ? tt : 0.0);
+  }
   __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
     if (tt > t) place(tt);
   }
@@ -262,6 +281,24 @@ struct Walker {
     rx = dir.z;
     ry = dir.w;
     place(0.0);
+  }
+  // emplace + seek(tt): place() resets the whole state, so one place at max(0, tt)
+  __device__ __forceinline__ void init_at(double x, double y, const double4& dir, double tt) {
+    ox = x;
+    oy = y;
+    dx = dir.x;
+    dy = dir.y;
+    rx = dir.z;
+    ry = dir.w;
+#if RL_WALK_BRANCHFREE
+    bx = dx > 0 ? 1.0 : 0.0;
+    by = dy > 0 ? 1.0 : 0.0;
+    sx = dx > 0 ? 1 : -1;
+    sy = dy > 0 ? 1 : -1;
+    zx = !(dx > 0) && !(dx < 0);
+    zy = !(dy > 0) && !(dy < 0);
+#endif
+    place(tt > 0.0 ? tt : 0.0);
   }
   __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
     if (tt > t) place(tt);
@@ -353,6 +390,34 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
 #undef RL_PRED
 }
 
+#ifndef RL_SAMPLED_SEARCH
+#define RL_SAMPLED_SEARCH 0
+#endif
+constexpr int kSampleShift = 4;  // one guide key per 16 zero points
+
+// partition_point over the row zp[lo, hi) using the guide keys zs[j] =
+// zp[16 j] that fall inside the row: a search over those (a few entries of a
+// small, L2-resident array) picks the 16-element block holding the partition
+// point, then one search inside the block. Two dependent rounds instead of
+// log2(n); the returned index is the same (a partition point is unique).
+__device__ __forceinline__ uint32_t partition_point_guided(const CddtView& c, uint32_t lo,
+                                                           uint32_t hi, double xq, bool forward) {
+  const uint32_t j0 = (lo + 15) >> kSampleShift;
+  const uint32_t j1 = hi > 0 ? (hi - 1) >> kSampleShift : 0;
+  if (hi <= lo || j0 > j1) return partition_point(c.zp + lo, hi - lo, xq, forward);
+  // number of guide keys in [j0, j1] satisfying the predicate
+  const uint32_t k = partition_point(c.zs + j0, j1 - j0 + 1, xq, forward);
+  uint32_t a, b;  // the partition point lies in [a, b] (global indices)
+  if (k == 0) {
+    a = lo;
+    b = j0 << kSampleShift;
+  } else {
+    a = ((j0 + k - 1) << kSampleShift) + 1;
+    b = k <= j1 - j0 ? (j0 + k) << kSampleShift : hi;
+  }
+  return (a - lo) + partition_point(c.zp + a, b - a, xq, forward);
+}
+
 // Outcome of one query beyond the range: the occupied cell that settled it
 // and the resolving zero point (what MarkSink::mark receives, cddt.cpp:249,259).
 struct CastOut {
@@ -431,7 +496,11 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   // std::upper_bound (forward, xq < double(v)) / std::lower_bound (backward,
   // double(v) < xq): the partition point of a monotone predicate over the
   // sorted row (cddt.hpp:106-131); any search order yields the same index.
+#if RL_SAMPLED_SEARCH
+  const uint32_t first = partition_point_guided(c, lo, hi, xq, forward);
+#else
   const uint32_t first = partition_point(v, hi - lo, xq, forward);
+#endif
   const int n = (int)(hi - lo);
   int idx = forward ? (int)first : (int)first - 1;
   const int step = forward ? 1 : -1;
@@ -455,6 +524,9 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
       }
     }
     // verification window around the candidate (cddt.cpp:254-261)
+#ifdef RL_DEBUG_NOWALK  // timing experiment only: results are wrong
+    continue;
+#endif
     if (!have_walker) {
       wk.init(x, y, dir);
       have_walker = true;
@@ -507,7 +579,11 @@ __device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double 
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   const uint32_t g = sp.row_base + (uint32_t)row;
   const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
+#if RL_SAMPLED_SEARCH
+  const uint32_t first = partition_point_guided(c, lo, hi, xq, forward);
+#else
   const uint32_t first = partition_point(c.zp + lo, hi - lo, xq, forward);
+#endif
   const int n = (int)(hi - lo);
   const int idx = forward ? (int)first : (int)first - 1;
   if (idx < 0 || idx >= n) {
@@ -534,6 +610,123 @@ __device__ __forceinline__ bool directional_cast_fast(const CddtView& c, double 
     }
   }
   return false;
+}
+
+}  // namespace rl
+
+namespace rl {
+
+// ---- split form of directional_cast for the deferred-walk batch kernel ----
+// Phase 1 runs cddt.cpp:207-269 up to the first point where a RayWalker is
+// needed: a non-clear origin (near-field walk) or a candidate whose landing
+// probe does not settle it (verification window). Phase 2 resumes exactly
+// there. Split and unsplit runs take the same decisions in the same order.
+struct WalkDefer {
+  uint32_t lo, n;  // CSR row of the query
+  int idx;         // candidate whose window walk is pending; -1: near field
+};
+
+__device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x, double y, int a,
+                                                    double* result, WalkDefer* def) {
+  const Floor fcx = floor2(x), fcy = floor2(y);
+  const int cxi = fcx.i, cyi = fcy.i;
+  if (!in_bounds(c, cxi, cyi)) {
+    *result = c.max_range;
+    return true;
+  }
+  const bool forward = a < c.S;
+  const int s = forward ? a : a - c.S;
+  const SliceParam sp = c.slices[s];
+  const double xq = x * sp.cos_t + y * sp.sin_t;
+  const double yq = -x * sp.sin_t + y * sp.cos_t + sp.y_offset;
+  int row = floor2(yq).i;
+  if (row < 0) row = 0;
+  if (row >= sp.bin_count) row = sp.bin_count - 1;
+  const uint32_t g = sp.row_base + (uint32_t)row;
+  const uint32_t lo = __ldg(c.row_off + g), hi = __ldg(c.row_off + g + 1);
+  const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
+  if ((w0.x >> (cxi & 31)) & 1u) {
+    *result = 0.0;
+    return true;
+  }
+  def->lo = lo;
+  def->n = hi - lo;
+  if (!((w0.y >> (cxi & 31)) & 1u)) {
+    def->idx = -1;  // near field needs the walker: phase 2 redoes the whole query
+    return false;
+  }
+#if RL_SAMPLED_SEARCH
+  const uint32_t first = partition_point_guided(c, lo, hi, xq, forward);
+#else
+  const uint32_t first = partition_point(c.zp + lo, hi - lo, xq, forward);
+#endif
+  const int n = (int)(hi - lo);
+  const int step = forward ? 1 : -1;
+  const double4 dir = c.dirs[a];
+  const double gw = (double)c.w, gh = (double)c.h;
+  OccCache oc;
+  for (int idx = forward ? (int)first : (int)first - 1; idx >= 0 && idx < n; idx += step) {
+    const double vv = (double)__ldg(c.zp + lo + idx);
+    const double d = forward ? vv - xq : xq - vv;
+    if (d >= c.max_range) break;
+    const double px = x + d * dir.x, py = y + d * dir.y;
+    if (px >= 0.0 && py >= 0.0 && px < gw && py < gh) {
+      const Floor flx = floor2(px), fly = floor2(py);
+      const double fx = px - flx.d, fy = py - fly.d;
+      if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
+          fy < 1.0 - kLatticeEps && oc.occ(c, flx.i, fly.i)) {
+        *result = d;
+        return true;
+      }
+    }
+    def->idx = idx;  // first verification window: hand over to phase 2
+    return false;
+  }
+  *result = c.max_range;
+  return true;
+}
+
+// Phase 2 for a deferred window: the walker does not exist yet (the origin
+// was clear), so emplace + seek(d - kVerifyHalf) is one place() at
+// max(0, d - kVerifyHalf); then the reference's candidate loop continues.
+__device__ __forceinline__ double directional_cast_resume(const CddtView& c, double x, double y,
+                                                          int a, const WalkDefer& def) {
+  const bool forward = a < c.S;
+  const int s = forward ? a : a - c.S;
+  const SliceParam sp = c.slices[s];
+  const double xq = x * sp.cos_t + y * sp.sin_t;
+  const double4 dir = c.dirs[a];
+  const double dx = dir.x, dy = dir.y;
+  const double gw = (double)c.w, gh = (double)c.h;
+  const float* __restrict__ v = c.zp + def.lo;
+  const int n = (int)def.n, step = forward ? 1 : -1;
+  OccCache oc;
+  Walker wk;
+  bool first = true;
+  for (int idx = def.idx; idx >= 0 && idx < n; idx += step) {
+    const double vv = (double)__ldg(v + idx);
+    const double d = forward ? vv - xq : xq - vv;
+    if (d >= c.max_range) break;
+    if (!first) {  // landing probe (phase 1 already ran it for def.idx)
+      const double px = x + d * dx, py = y + d * dy;
+      if (px >= 0.0 && py >= 0.0 && px < gw && py < gh) {
+        const Floor flx = floor2(px), fly = floor2(py);
+        const double fx = px - flx.d, fy = py - fly.d;
+        if (fx > kLatticeEps && fx < 1.0 - kLatticeEps && fy > kLatticeEps &&
+            fy < 1.0 - kLatticeEps && oc.occ(c, flx.i, fly.i))
+          return d;
+      }
+      wk.seek(d - kVerifyHalf);
+    } else {
+      wk.init_at(x, y, dir, d - kVerifyHalf);
+      first = false;
+    }
+    const double r = wk.scan_to(c, oc, d + kVerifyHalf);
+    if (r == kWalkExit) break;
+    if (r < 0.0) continue;
+    return d;
+  }
+  return c.max_range;
 }
 
 }  // namespace rl

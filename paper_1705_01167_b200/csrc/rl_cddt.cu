@@ -179,6 +179,23 @@ __global__ void k_rowbits(const uint8_t* __restrict__ flags, int w, int h, int w
   }
 }
 
+__global__ void k_guide(const float* __restrict__ zp, size_t n, float* __restrict__ zs) {
+  const size_t m = (n + 15) >> 4;
+  for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < m;
+       j += size_t(gridDim.x) * blockDim.x)
+    zs[j] = zp[j << 4];
+}
+
+int refresh_guide(rl_cddt* c) {
+  const size_t m = (c->zero_points + 15) / 16;
+  if (c->zs.n < m || c->zs.n == 0) RL_TRY(c->zs.alloc(m));
+  if (m)
+    k_guide<<<int(std::min<size_t>((m + 255) / 256, size_t(sm_count()) * 16)), 256, 0,
+              c->stream>>>(c->zp.p, c->zero_points, c->zs.p);
+  RL_CK(cudaGetLastError());
+  return RL_OK;
+}
+
 int refresh_tiles(rl_cddt* c) {
   c->wpr = (c->w + 31) / 32;
   const size_t nw = size_t(c->wpr) * c->h;
@@ -349,6 +366,7 @@ int build_structure(rl_cddt* c) {
                                              int(rows), c->row_off.p, c->row_off.p + 1, st));
   }
   RL_TRY(refresh_tiles(c));
+  RL_TRY(refresh_guide(c));
   // host membership mirror
   c->member_h.assign(wh, 0);
   {
@@ -483,6 +501,116 @@ __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast_p2(CddtView c,
   }
 }
 
+#ifndef RL_DEFER_WALK
+#define RL_DEFER_WALK 1
+#endif
+// Deferred-walk batch (the f32, no-extras entry point). Phase 1 settles
+// every query that needs no RayWalker (about two thirds at config 3) with
+// uniform control flow, and queues the rest — with the CSR row and the
+// pending candidate — through a per-CTA shared-memory compaction (one global
+// atomic per CTA iteration). Phase 2 resumes only those queries, so the
+// divergent walker code runs with lanes that all need it.
+struct __align__(16) WalkRecord {
+  float x, y, t;
+  uint32_t i, lo, n;
+  int32_t idx, pad;
+};
+
+#ifndef RL_P1_MINB
+#define RL_P1_MINB 4
+#endif
+#ifndef RL_P2_MINB
+#define RL_P2_MINB 4
+#endif
+template <class T>
+__global__ void __launch_bounds__(256, RL_P1_MINB) k_cast_defer_p1(
+    CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
+    T* __restrict__ out, uint32_t n, WalkRecord* __restrict__ q, unsigned* __restrict__ qn) {
+  // queue layout: window records grow up from q[0], near-field records down
+  // from q[n-1]; qn[0], qn[1] count them
+  __shared__ unsigned cnt_s[2][8], base_s[2];
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n; b0 += gridDim.x * blockDim.x) {
+    const uint32_t i = b0 + threadIdx.x;
+    bool defer = false;
+    WalkRecord rec;
+    if (i < n) {
+      rec.x = __ldcs(qx + i);
+      rec.y = __ldcs(qy + i);
+      rec.t = __ldcs(qt + i);
+      rec.i = i;
+      const double th = normalize_angle_2pi(double(rec.t));
+      double r;
+      WalkDefer def;
+      if (directional_cast_p1(c, double(rec.x), double(rec.y), direction_index(th, c.K), &r,
+                              &def)) {
+        __stcs(out + i, T(r));
+      } else {
+        defer = true;
+        rec.lo = def.lo;
+        rec.n = def.n;
+        rec.idx = def.idx;
+        rec.pad = 0;
+      }
+    }
+    const bool near = defer && rec.idx < 0, win = defer && !near;
+    const unsigned bw = __ballot_sync(0xffffffffu, win), bn = __ballot_sync(0xffffffffu, near);
+    if (lane == 0) {
+      cnt_s[0][wid] = __popc(bw);
+      cnt_s[1][wid] = __popc(bn);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      unsigned tot = 0;
+      for (int w = 0; w < 8; w++) {
+        const unsigned k = cnt_s[threadIdx.x][w];
+        cnt_s[threadIdx.x][w] = tot;
+        tot += k;
+      }
+      base_s[threadIdx.x] = tot ? atomicAdd(qn + threadIdx.x, tot) : 0u;
+    }
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1;
+    if (defer) {  // records are touched twice: stream them past L2 (evict-first)
+      const size_t slot = win ? base_s[0] + cnt_s[0][wid] + __popc(bw & below)
+                              : n - 1 - (base_s[1] + cnt_s[1][wid] + __popc(bn & below));
+      const float4* src = reinterpret_cast<const float4*>(&rec);
+      float4* dst = reinterpret_cast<float4*>(q + slot);
+      __stcs(dst, src[0]);
+      __stcs(dst + 1, src[1]);
+    }
+    __syncthreads();
+  }
+}
+
+// NEAR: records whose origin needs the near-field walk, redone in full;
+// otherwise the pending verification windows, resumed in place.
+template <class T, bool NEAR>
+__global__ void __launch_bounds__(256, RL_P2_MINB) k_cast_defer_p2(
+    CddtView c, const WalkRecord* __restrict__ q, const unsigned* __restrict__ qn, uint32_t n,
+    T* __restrict__ out) {
+  const unsigned m = qn[NEAR ? 1 : 0];
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+    WalkRecord r;
+    {
+      const float4* src = reinterpret_cast<const float4*>(q + (NEAR ? n - 1 - k : k));
+      float4* dst = reinterpret_cast<float4*>(&r);
+      dst[0] = __ldcs(src);
+      dst[1] = __ldcs(src + 1);
+    }
+    const double x = double(r.x), y = double(r.y);
+    const int a = direction_index(normalize_angle_2pi(double(r.t)), c.K);
+    double res;
+    if (NEAR) {
+      CastOut o;
+      res = directional_cast(c, x, y, a, o);
+    } else {
+      res = directional_cast_resume(c, x, y, a, WalkDefer{r.lo, r.n, r.idx});
+    }
+    __stcs(out + r.i, T(res));
+  }
+}
+
 // One full wave: every SM holds as many 256-thread CTAs as registers allow
 // and the grid-stride loop spreads the queries evenly (no partial last wave).
 template <class T, class I, bool HIT, bool RES>
@@ -569,7 +697,30 @@ static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T*
 #else
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
-#if RL_TWO_PHASE
+#if RL_DEFER_WALK
+  if (!rr && !ri && !hit && small) {
+    rl_cddt* cm = const_cast<rl_cddt*>(c);
+    const size_t need = sizeof(WalkRecord) * n + 256;
+    if (cm->defer_ws.n < need) cm->defer_ws.alloc(need);
+    unsigned* qn = reinterpret_cast<unsigned*>(cm->defer_ws.p);
+    WalkRecord* q = reinterpret_cast<WalkRecord*>(cm->defer_ws.p + 256);
+    cudaMemsetAsync(qn, 0, 2 * sizeof(unsigned), st);
+    static int p1 = 0, p2 = 0, p3 = 0;
+    if (!p1) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_cast_defer_p1<T>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_cast_defer_p2<T, false>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p3, k_cast_defer_p2<T, true>, 256, 0);
+      p1 = std::max(p1, 1);
+      p2 = std::max(p2, 1);
+      p3 = std::max(p3, 1);
+    }
+    const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
+    k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
+    k_cast_defer_p2<T, false><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+    k_cast_defer_p2<T, true><<<sm_count() * p3, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+    return;
+  }
+#elif RL_TWO_PHASE
   if (!rr && !ri && !hit && small) {
     rl_cddt* cm = const_cast<rl_cddt*>(c);
     const size_t need = sizeof(DeferredQuery) * n + 256;
@@ -715,6 +866,8 @@ int prune_structure(rl_cddt* c) {
   c->row_off = std::move(noff);
   c->zero_points = kept;
   c->pruned = true;
+  RL_TRY(refresh_guide(c));
+  RL_CK(cudaStreamSynchronize(st));
   return RL_OK;
 }
 
@@ -805,6 +958,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->rowbits.release();
     c->row_off.release();
     c->zp.release();
+    c->zs.release();
     c->d_slices.release();
     c->d_dirs.release();
     c->d_scalar.release();

@@ -117,6 +117,7 @@ struct rl_cddt {
   int wpr = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
   rl::DevBuf<float> zp;             // capacity >= zero_points
+  rl::DevBuf<float> zs;             // search guide zs[j] = zp[16 j]
   rl::DevBuf<rl::SliceParam> d_slices;
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
@@ -132,6 +133,7 @@ struct rl_cddt {
     v.wpr = wpr;
     v.row_off = row_off.p;
     v.zp = zp.p;
+    v.zs = zs.p;
     v.slices = d_slices.p;
     v.dirs = d_dirs.p;
     v.w = w;
@@ -151,4 +153,5 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
 }
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_tiles(rl_cddt* c);          // rebuild query tiles from flags
+int refresh_guide(rl_cddt* c);          // rebuild the search guide from zp
 }  // namespace rl

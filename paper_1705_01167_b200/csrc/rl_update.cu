@@ -300,6 +300,8 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   c->zp = std::move(nzp);
   c->row_off = std::move(new_off);
   c->zero_points = total;
+  RL_TRY(refresh_guide(c));
+  RL_CK(cudaStreamSynchronize(st));
   return RL_OK;
 }
 
