@@ -187,6 +187,7 @@ __global__ void k_guide(const float* __restrict__ zp, size_t n, float* __restric
 }
 
 int refresh_guide(rl_cddt* c) {
+  if (!RL_SAMPLED_SEARCH) return RL_OK;
   const size_t m = (c->zero_points + 15) / 16;
   if (c->zs.n < m || c->zs.n == 0) RL_TRY(c->zs.alloc(m));
   if (m)
@@ -698,7 +699,8 @@ static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T*
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
 #if RL_DEFER_WALK
-  if (!rr && !ri && !hit && small) {
+  // small batches (a few waves) gain nothing from the split and pay two more launches
+  if (!rr && !ri && !hit && small && n >= (size_t(1) << 22)) {
     rl_cddt* cm = const_cast<rl_cddt*>(c);
     const size_t need = sizeof(WalkRecord) * n + 256;
     if (cm->defer_ws.n < need) cm->defer_ws.alloc(need);
