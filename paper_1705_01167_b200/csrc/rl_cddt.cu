@@ -966,6 +966,9 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->d_scalar.release();
     c->ws.release();
     c->defer_ws.release();
+    c->upd_ws.release();
+    c->zp_spare.release();
+    c->off_spare.release();
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;

@@ -123,6 +123,9 @@ struct rl_cddt {
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
   rl::DevBuf<uint8_t> defer_ws;     // two-phase cast: deferred-query records
+  rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
+  rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
+  rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off
 
   rl::CddtView view() const {
     rl::CddtView v;

@@ -219,90 +219,90 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
     }
   }
   cudaStream_t st = c->stream;
-  DevBuf<int32_t> d_wcells;
-  DevBuf<uint8_t> d_wflags;
-  RL_TRY(d_wcells.alloc(wcells.size()));
-  RL_TRY(d_wflags.alloc(wflags.size()));
-  RL_CK(cudaMemcpyAsync(d_wcells.p, wcells.data(), 4 * wcells.size(), cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemcpyAsync(d_wflags.p, wflags.data(), wflags.size(), cudaMemcpyHostToDevice, st));
-  k_set_flags<<<blocks_for(wcells.size(), 256), 256, 0, st>>>(d_wcells.p, d_wflags.p,
-                                                              int(wcells.size()), c->flags.p);
-  RL_CK(cudaGetLastError());
-  RL_TRY(refresh_tiles(c));
-  if (dcells.empty()) return RL_OK;
-
-  // 3. delta records
+  const size_t nw = wcells.size();
   const int nd = int(dcells.size());
   const size_t cap = size_t(nd) * c->S * 3;  // a unit square spans at most 3 rows
-  DevBuf<int32_t> d_dcells, add_cnt, rem_cnt;
-  DevBuf<int8_t> d_dsign, vals, vals_sorted;
-  DevBuf<unsigned long long> keys, keys_sorted;
-  DevBuf<unsigned> d_count;
-  RL_TRY(d_dcells.alloc(nd));
-  RL_TRY(d_dsign.alloc(nd));
-  RL_TRY(add_cnt.alloc(c->rows));
-  RL_TRY(rem_cnt.alloc(c->rows));
-  RL_TRY(keys.alloc(cap));
-  RL_TRY(vals.alloc(cap));
-  RL_TRY(keys_sorted.alloc(cap));
-  RL_TRY(vals_sorted.alloc(cap));
-  RL_TRY(d_count.alloc(2));
-  RL_CK(cudaMemcpyAsync(d_dcells.p, dcells.data(), 4 * nd, cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemcpyAsync(d_dsign.p, dsign.data(), nd, cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemsetAsync(add_cnt.p, 0, 4 * c->rows, st));
-  RL_CK(cudaMemsetAsync(rem_cnt.p, 0, 4 * c->rows, st));
-  RL_CK(cudaMemsetAsync(d_count.p, 0, 8, st));
+  const size_t rows = c->rows;
+  // one persistent workspace, carved in 256-byte aligned pieces
+  size_t sort_tmp = 0, scan_tmp = 0;
+  if (nd) {
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, (int8_t*)nullptr,
+                                    (int8_t*)nullptr, int(cap), 0, 64, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  int(rows + 1), st);
+  }
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd), 4 * rows, 4 * rows, 8 * cap,
+                          cap, 8 * cap, cap, 8, 4 * (rows + 1), std::max(sort_tmp, scan_tmp)};
+  size_t need = 0;
+  for (size_t b : sizes) need += al(b);
+  if (c->upd_ws.n < need) RL_TRY(c->upd_ws.alloc(need + need / 4));
+  uint8_t* cur = c->upd_ws.p;
+  auto take = [&](size_t b) {
+    uint8_t* p = cur;
+    cur += al(b);
+    return p;
+  };
+  int32_t* d_wcells = reinterpret_cast<int32_t*>(take(sizes[0]));
+  uint8_t* d_wflags = take(sizes[1]);
+  int32_t* d_dcells = reinterpret_cast<int32_t*>(take(sizes[2]));
+  int8_t* d_dsign = reinterpret_cast<int8_t*>(take(sizes[3]));
+  int32_t* add_cnt = reinterpret_cast<int32_t*>(take(sizes[4]));
+  int32_t* rem_cnt = reinterpret_cast<int32_t*>(take(sizes[5]));
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(take(sizes[6]));
+  int8_t* vals = reinterpret_cast<int8_t*>(take(sizes[7]));
+  unsigned long long* keys_sorted = reinterpret_cast<unsigned long long*>(take(sizes[8]));
+  int8_t* vals_sorted = reinterpret_cast<int8_t*>(take(sizes[9]));
+  unsigned* d_count = reinterpret_cast<unsigned*>(take(sizes[10]));
+  uint32_t* len = reinterpret_cast<uint32_t*>(take(sizes[11]));
+  void* tmp = take(sizes[12]);
+
+  RL_CK(cudaMemcpyAsync(d_wcells, wcells.data(), 4 * nw, cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemcpyAsync(d_wflags, wflags.data(), nw, cudaMemcpyHostToDevice, st));
+  k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(d_wcells, d_wflags, int(nw), c->flags.p);
+  RL_CK(cudaGetLastError());
+  RL_TRY(refresh_tiles(c));
+  if (nd == 0) return finish(c, nullptr);
+
+  // 3. delta records; unused key slots stay at UINT64_MAX and sort last, so
+  //    the fixed-size sort needs no host round trip for the record count
+  RL_CK(cudaMemcpyAsync(d_dcells, dcells.data(), 4 * size_t(nd), cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemcpyAsync(d_dsign, dsign.data(), size_t(nd), cudaMemcpyHostToDevice, st));
+  RL_CK(cudaMemsetAsync(add_cnt, 0, 4 * rows, st));
+  RL_CK(cudaMemsetAsync(rem_cnt, 0, 4 * rows, st));
+  RL_CK(cudaMemsetAsync(d_count, 0, 8, st));
+  RL_CK(cudaMemsetAsync(keys, 0xFF, 8 * cap, st));
   k_delta_records<<<blocks_for(size_t(nd) * c->S, 256), 256, 0, st>>>(
-      d_dcells.p, d_dsign.p, nd, c->d_slices.p, c->S, w, keys.p, vals.p, d_count.p, add_cnt.p,
-      rem_cnt.p);
+      d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, keys, vals, d_count, add_cnt, rem_cnt);
   RL_CK(cudaGetLastError());
-  unsigned n_rec = 0;
-  RL_CK(cudaMemcpyAsync(&n_rec, d_count.p, 4, cudaMemcpyDeviceToHost, st));
-  RL_CK(cudaStreamSynchronize(st));
-  {
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, vals.p,
-                                    vals_sorted.p, int(n_rec), 0, 64, st);
-    DevBuf<uint8_t> tmp;
-    RL_TRY(tmp.alloc(tmp_bytes));
-    RL_CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_sorted.p, vals.p,
-                                          vals_sorted.p, int(n_rec), 0, 64, st));
-  }
-  // 4. new offsets and merge
-  DevBuf<uint32_t> len, new_off;
-  RL_TRY(len.alloc(c->rows + 1));
-  RL_TRY(new_off.alloc(c->rows + 1));
-  k_new_len<<<blocks_for(c->rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt.p, rem_cnt.p,
-                                                          len.p, c->rows);
-  {
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, len.p, new_off.p, int(c->rows + 1), st);
-    DevBuf<uint8_t> tmp;
-    RL_TRY(tmp.alloc(tmp_bytes));
-    RL_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, len.p, new_off.p, int(c->rows + 1), st));
-  }
-  uint32_t total = 0;
-  RL_CK(cudaMemcpyAsync(&total, new_off.p + c->rows, 4, cudaMemcpyDeviceToHost, st));
-  RL_CK(cudaStreamSynchronize(st));
-  DevBuf<float> nzp;
-  RL_TRY(nzp.alloc(total));
-  k_merge_rows<<<blocks_for(c->rows * 32, 256, 32), 256, 0, st>>>(
-      c->row_off.p, c->zp.p, new_off.p, nzp.p, add_cnt.p, rem_cnt.p, keys_sorted.p, vals_sorted.p,
-      n_rec, c->rows, d_count.p + 1);
+  RL_CK(cub::DeviceRadixSort::SortPairs(tmp, sort_tmp, keys, keys_sorted, vals, vals_sorted,
+                                        int(cap), 0, 64, st));
+  // 4. new offsets and merge into the spare buffers, then swap
+  if (c->off_spare.n < rows + 1) RL_TRY(c->off_spare.alloc(rows + 1));
+  const size_t zp_need = c->zero_points + cap;
+  if (c->zp_spare.n < zp_need) RL_TRY(c->zp_spare.alloc(zp_need + zp_need / 8));
+  uint32_t* new_off = c->off_spare.p;
+  k_new_len<<<blocks_for(rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt, rem_cnt, len, rows);
+  RL_CK(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp, len, new_off, int(rows + 1), st));
+  k_merge_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(
+      c->row_off.p, c->zp.p, new_off, c->zp_spare.p, add_cnt, rem_cnt, keys_sorted, vals_sorted,
+      unsigned(cap), rows, d_count + 1);
   RL_CK(cudaGetLastError());
-  unsigned miss = 0;
-  RL_CK(cudaMemcpyAsync(&miss, d_count.p + 1, 4, cudaMemcpyDeviceToHost, st));
+  uint32_t total_miss[2] = {0, 0};
+  RL_CK(cudaMemcpyAsync(&total_miss[0], new_off + rows, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaMemcpyAsync(&total_miss[1], d_count + 1, 4, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
-  if (miss) {
-    set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)", miss);
+  if (total_miss[1]) {
+    set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)",
+              total_miss[1]);
     return RL_ELOGIC;
   }
-  c->zp = std::move(nzp);
-  c->row_off = std::move(new_off);
-  c->zero_points = total;
+  std::swap(c->zp, c->zp_spare);
+  std::swap(c->row_off, c->off_spare);
+  c->zero_points = total_miss[0];
   RL_TRY(refresh_guide(c));
-  RL_CK(cudaStreamSynchronize(st));
-  return RL_OK;
+  return finish(c, nullptr);
 }
 
 }  // namespace rl
