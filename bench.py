@@ -121,15 +121,27 @@ def profile_traffic():
     return None
 
 
-def make_workload(n_queries: int, rank: int):
+def make_workload(n_queries: int, rank: int, on_gpu: bool = True):
+    """The config-3 map and this rank's query slice in pinned host memory.
+    On a GPU the queries come from the device twin of the generator (bit-identical
+    to synth.free_queries, tests/test_gpu_synth.py) — seconds of host time per
+    rank otherwise."""
     import numpy as np
     import torch
 
     from paper_1705_01167_b200 import synth
     g = synth.polygon_map(4000, 4000, 0.12, seed=3)
     qx, qy, qt = (torch.empty(n_queries, dtype=torch.float32).pin_memory() for _ in range(3))
-    synth.free_queries(g, n_queries, seed=7, start=rank * n_queries,
-                       out=(qx.numpy(), qy.numpy(), qt.numpy()))
+    if on_gpu and torch.cuda.is_available():
+        gd = torch.from_numpy(g).cuda()
+        dq = synth.free_queries_gpu(gd, 4000, 4000, n_queries, seed=7, start=rank * n_queries)
+        for h, d in zip((qx, qy, qt), dq):
+            h.copy_(d)
+        del dq, gd
+        torch.cuda.synchronize()
+    else:
+        synth.free_queries(g, n_queries, seed=7, start=rank * n_queries,
+                           out=(qx.numpy(), qy.numpy(), qt.numpy()))
     return g, qx, qy, qt, np
 
 
@@ -403,7 +415,7 @@ def run_ours(args, rank, world, local_rank):
 def run_reference(args):
     """--impl reference: the unmodified reference on the host cores, rank 0 only."""
     n = args.ref_sample
-    g, qx, qy, qt, np = make_workload(n, 0)
+    g, qx, qy, qt, np = make_workload(n, 0, on_gpu=False)
     threads = os.cpu_count() or 1
     import oracle
     oracle.build(ref=True)

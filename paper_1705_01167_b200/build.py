@@ -23,6 +23,7 @@ CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "librl_cddt.so"
 SYNTH = PKG / "libcddt_synth.so"
+SYNTH_GPU = PKG / "libcddt_synth_gpu.so"
 OBJ = PKG / "build"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,7 +59,7 @@ def _run(cmd: list[str], log: Path | None = None) -> None:
 def build_cuda(force: bool = False, defines: tuple[str, ...] = (), out: Path | None = None) -> Path:
     """Build librl_cddt.so (or, with `defines`, a variant library at `out`)."""
     lib = out or LIB
-    cu = sorted(CSRC.glob("*.cu"))
+    cu = sorted(p for p in CSRC.glob("*.cu") if p.name != "synth_gpu.cu")
     hdrs = sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
     if not force and not _stale(lib, cu + hdrs + [Path(__file__)]):
         return lib
@@ -94,8 +95,22 @@ def build_synth(force: bool = False) -> Path:
     return SYNTH
 
 
+def build_synth_gpu(force: bool = False) -> Path:
+    """Device twin of the query generator (harness side, not the C ABI)."""
+    src = CSRC / "synth_gpu.cu"
+    if not force and not _stale(SYNTH_GPU, [src]):
+        return SYNTH_GPU
+    tmp = SYNTH_GPU.with_suffix(".so.tmp")
+    _run([_nvcc(), *ARCH, "-std=c++17", "-O3", "-Xcompiler", "-fPIC,-ffp-contract=off",
+          "-fmad=false", "-shared", "-o", str(tmp), str(src), "-lcudart_static", "-lrt", "-ldl",
+          "-lpthread"])
+    os.replace(tmp, SYNTH_GPU)
+    return SYNTH_GPU
+
+
 def build_all(force: bool = False) -> None:
     build_synth(force)
+    build_synth_gpu(force)
     build_cuda(force)
 
 

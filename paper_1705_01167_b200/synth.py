@@ -40,6 +40,31 @@ def lib() -> C.CDLL:
     return _lib
 
 
+_gpu = None
+
+
+def free_queries_gpu(grid_dev, w: int, h: int, n: int, seed=7, start=0, out=None):
+    """Device twin of free_queries (csrc/synth_gpu.cu): identical bits, generated on
+    the current CUDA device. grid_dev: torch uint8 CUDA tensor [h, w]."""
+    import torch
+    global _gpu
+    if _gpu is None:
+        from .build import SYNTH_GPU, build_synth_gpu
+        if not SYNTH_GPU.exists():
+            build_synth_gpu()
+        _gpu = C.CDLL(str(SYNTH_GPU))
+        _gpu.synth_free_queries_gpu.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_uint64,
+                                                C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]
+    if out is None:
+        out = tuple(torch.empty(n, dtype=torch.float32, device=grid_dev.device) for _ in range(3))
+    qx, qy, qt = out
+    stream = C.c_void_p(torch.cuda.current_stream(grid_dev.device).cuda_stream)
+    assert _gpu.synth_free_queries_gpu(grid_dev.data_ptr(), w, h, seed, start, n, qx.data_ptr(),
+                                       qy.data_ptr(), qt.data_ptr(), stream) == 0
+    return qx, qy, qt
+
+
 def rect_map(w=500, h=500, nrect=40, seed=2) -> np.ndarray:
     """Config 1: border + nrect rectangles (side 5-60 px)."""
     g = np.zeros((h, w), dtype=np.uint8)
