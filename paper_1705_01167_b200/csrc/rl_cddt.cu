@@ -19,7 +19,6 @@
 #include <cmath>
 #include <cstring>
 
-#include "cddt_cast_sm.cuh"
 #include "rl_common.cuh"
 
 namespace rl {
@@ -141,29 +140,7 @@ __global__ void k_flags(const uint8_t* __restrict__ grid, uint8_t* __restrict__ 
   }
 }
 
-// Query tiles: 8x8 cells per tile, occupied and clear bits (cddt_device.cuh).
-__global__ void k_tiles(const uint8_t* __restrict__ flags, int w, int h, int tw, int th,
-                        ulonglong2* __restrict__ tiles) {
-  const int n = tw * th;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-    const int x0 = (t % tw) * 8, y0 = (t / tw) * 8;
-    unsigned long long occ = 0, clr = 0;
-    for (int dy = 0; dy < 8; dy++) {
-      const int y = y0 + dy;
-      if (y >= h) break;
-      for (int dx = 0; dx < 8; dx++) {
-        const int x = x0 + dx;
-        if (x >= w) break;
-        const uint8_t f = flags[size_t(y) * w + x];
-        const int b = dy * 8 + dx;
-        if (f & kOcc) occ |= 1ull << b;
-        if (f & kClear) clr |= 1ull << b;
-      }
-    }
-    tiles[t] = make_ulonglong2(occ, clr);
-  }
-}
-
+// Query occupancy bits: per 32-cell run of a grid row, {occupied, clear}.
 __global__ void k_rowbits(const uint8_t* __restrict__ flags, int w, int h, int wpr,
                           uint2* __restrict__ bits) {
   const int n = wpr * h;
@@ -179,37 +156,12 @@ __global__ void k_rowbits(const uint8_t* __restrict__ flags, int w, int h, int w
   }
 }
 
-__global__ void k_guide(const float* __restrict__ zp, size_t n, float* __restrict__ zs) {
-  const size_t m = (n + 15) >> 4;
-  for (size_t j = blockIdx.x * size_t(blockDim.x) + threadIdx.x; j < m;
-       j += size_t(gridDim.x) * blockDim.x)
-    zs[j] = zp[j << 4];
-}
-
-int refresh_guide(rl_cddt* c) {
-  if (!RL_SAMPLED_SEARCH) return RL_OK;
-  const size_t m = (c->zero_points + 15) / 16;
-  if (c->zs.n < m || c->zs.n == 0) RL_TRY(c->zs.alloc(m));
-  if (m)
-    k_guide<<<int(std::min<size_t>((m + 255) / 256, size_t(sm_count()) * 16)), 256, 0,
-              c->stream>>>(c->zp.p, c->zero_points, c->zs.p);
-  RL_CK(cudaGetLastError());
-  return RL_OK;
-}
-
-int refresh_tiles(rl_cddt* c) {
+int refresh_query_bits(rl_cddt* c) {
   c->wpr = (c->w + 31) / 32;
   const size_t nw = size_t(c->wpr) * c->h;
   if (c->rowbits.n != nw) RL_TRY(c->rowbits.alloc(nw));
   k_rowbits<<<int(std::min<size_t>((nw + 255) / 256, size_t(sm_count()) * 16)), 256, 0,
               c->stream>>>(c->flags.p, c->w, c->h, c->wpr, c->rowbits.p);
-  RL_CK(cudaGetLastError());
-  c->tw = (c->w + 7) / 8;
-  c->th = (c->h + 7) / 8;
-  const size_t n = size_t(c->tw) * c->th;
-  if (c->tiles.n != n) RL_TRY(c->tiles.alloc(n));
-  k_tiles<<<int(std::min<size_t>((n + 255) / 256, size_t(sm_count()) * 16)), 256, 0, c->stream>>>(
-      c->flags.p, c->w, c->h, c->tw, c->th, c->tiles.p);
   RL_CK(cudaGetLastError());
   return RL_OK;
 }
@@ -366,8 +318,7 @@ int build_structure(rl_cddt* c) {
     RL_CK(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, unsorted.p, c->zp.p, int(total),
                                              int(rows), c->row_off.p, c->row_off.p + 1, st));
   }
-  RL_TRY(refresh_tiles(c));
-  RL_TRY(refresh_guide(c));
+  RL_TRY(refresh_query_bits(c));
   // host membership mirror
   c->member_h.assign(wh, 0);
   {
@@ -380,62 +331,26 @@ int build_structure(rl_cddt* c) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: batched casts, one thread per query, grid-stride.
-#ifndef RL_L2_PERSIST
-#define RL_L2_PERSIST 0
-#endif
-#ifndef RL_PREFETCH
-#define RL_PREFETCH 0
-#endif
-#ifndef RL_STREAM_IO
-#define RL_STREAM_IO 1
-#endif
-#ifndef RL_GRID_PER_SM
-#define RL_GRID_PER_SM 0  // 0: one full wave from the occupancy calculator
-#endif
-#ifndef RL_CAST_MINB
-#define RL_CAST_MINB 4  // resident 256-thread CTAs per SM the register budget targets
-#endif
+// K3: batched casts.
+//
+// Monolithic form (f64 / hit-cell / resolving-index outputs, and batches
+// below 4M queries): one thread per query, grid-stride, a single full wave
+// sized by the occupancy calculator (4 x 256-thread CTAs per SM at 64 regs).
 template <class T, class I, bool HIT, bool RES>
-__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T* __restrict__ qx,
-                                              const T* __restrict__ qy, const T* __restrict__ qt,
-                                              T* __restrict__ out, int32_t* __restrict__ hit,
-                                              int64_t* __restrict__ res_row,
-                                              int32_t* __restrict__ res_idx, I n) {
-  const I stride = I(gridDim.x) * I(blockDim.x);
-  I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x);
-#if RL_PREFETCH
-  // software pipeline: the next query's inputs are requested while the
-  // current one walks its dependent gathers, hiding the DRAM stream latency
-  T nx = T(0), ny = T(0), nt = T(0);
-  if (i < n) {
-    nx = __ldcs(qx + i);
-    ny = __ldcs(qy + i);
-    nt = __ldcs(qt + i);
-  }
-#endif
-  for (; i < n; i += stride) {
-#if RL_PREFETCH
-    const double x = double(nx), y = double(ny);
-    const double th = normalize_angle_2pi(double(nt));  // RayQuery ctor, raycast.hpp:47
-    if (i + stride < n) {
-      nx = __ldcs(qx + i + stride);
-      ny = __ldcs(qy + i + stride);
-      nt = __ldcs(qt + i + stride);
-    }
-#else
+__global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict__ qx,
+                                                 const T* __restrict__ qy,
+                                                 const T* __restrict__ qt, T* __restrict__ out,
+                                                 int32_t* __restrict__ hit,
+                                                 int64_t* __restrict__ res_row,
+                                                 int32_t* __restrict__ res_idx, I n) {
+  for (I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); i < n;
+       i += I(gridDim.x) * I(blockDim.x)) {
     // query streams are touched once: evict-first so the structure stays in L2
     const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
     const double th = normalize_angle_2pi(double(__ldcs(qt + i)));  // RayQuery ctor, raycast.hpp:47
-#endif
-    const int a = direction_index(th, c.K);
     CastOut o;
-    const double r = directional_cast(c, x, y, a, o);
-#if RL_STREAM_IO
+    const double r = directional_cast(c, x, y, direction_index(th, c.K), o);
     if (out) __stcs(out + i, T(r));
-#else
-    if (out) out[i] = T(r);
-#endif
     if (HIT) hit[i] = o.hit;
     if (RES) {
       if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
@@ -444,87 +359,30 @@ __global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast(CddtView c, const T*
   }
 }
 
-#ifndef RL_TWO_PHASE
-#define RL_TWO_PHASE 0
-#endif
-// Two-phase batch: phase 1 settles every query that needs no RayWalker with
-// straight-line code (high SIMT efficiency) and appends the rest as compact
-// (x, y, theta, index) records; phase 2 runs the full directional_cast over
-// those records only, so the divergent walker code runs with lanes that all
-// need it.
-struct DeferredQuery {
-  float x, y, t;
-  uint32_t i;
-};
-
-template <class T>
-__global__ void __launch_bounds__(256) k_cast_p1(CddtView c, const T* __restrict__ qx,
-                                                 const T* __restrict__ qy,
-                                                 const T* __restrict__ qt, T* __restrict__ out,
-                                                 uint32_t n, DeferredQuery* __restrict__ q,
-                                                 unsigned* __restrict__ qn) {
-  const unsigned lane = threadIdx.x & 31;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
-    bool defer = false;
-    float fx = 0, fy = 0, ft = 0;
-    if (i < n) {
-      fx = __ldcs(qx + i);
-      fy = __ldcs(qy + i);
-      ft = __ldcs(qt + i);
-      const double th = normalize_angle_2pi(double(ft));
-      double r;
-      if (directional_cast_fast(c, double(fx), double(fy), direction_index(th, c.K), &r))
-        __stcs(out + i, T(r));
-      else
-        defer = true;
-    }
-    const unsigned ballot = __ballot_sync(0xffffffffu, defer);
-    unsigned pos0 = 0;
-    if (lane == 0 && ballot) pos0 = atomicAdd(qn, __popc(ballot));
-    pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-    if (defer) q[pos0 + __popc(ballot & ((1u << lane) - 1))] = DeferredQuery{fx, fy, ft, i};
-  }
-}
-
-template <class T>
-__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast_p2(CddtView c,
-                                                               const DeferredQuery* __restrict__ q,
-                                                               const unsigned* __restrict__ qn,
-                                                               T* __restrict__ out) {
-  const unsigned m = *qn;
-  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
-    const DeferredQuery d = q[k];
-    const double th = normalize_angle_2pi(double(d.t));
-    CastOut o;
-    const double r = directional_cast(c, double(d.x), double(d.y), direction_index(th, c.K), o);
-    __stcs(out + d.i, T(r));
-  }
-}
-
-#ifndef RL_DEFER_WALK
-#define RL_DEFER_WALK 1
-#endif
-// Deferred-walk batch (the f32, no-extras entry point). Phase 1 settles
-// every query that needs no RayWalker (about two thirds at config 3) with
-// uniform control flow, and queues the rest — with the CSR row and the
-// pending candidate — through a per-CTA shared-memory compaction (one global
-// atomic per CTA iteration). Phase 2 resumes only those queries, so the
-// divergent walker code runs with lanes that all need it.
+// Deferred-walk form (f32 ranges only, >= 4M queries; the bench path).
+// About a third of the queries need a RayWalker (a near-field walk or a
+// verification window). Run inline, those walks execute with ~5 of 32 lanes
+// active and cost half the kernel time (profiles/r01/ncu_k_cast_v3.txt).
+// Phase 1 settles every query that needs no walker with uniform control flow
+// and queues the rest — with the CSR row and the pending candidate — through
+// a per-CTA shared-memory compaction (one global atomic per CTA iteration).
+// Phase 2 resumes exactly there (cddt_device.cuh directional_cast_resume),
+// with every lane walking; near-field queries are redone in full by a third
+// launch. Records are streamed evict-first past L2.
 struct __align__(16) WalkRecord {
   float x, y, t;
   uint32_t i, lo, n;
   int32_t idx, pad;
 };
 
-#ifndef RL_P1_MINB
-#define RL_P1_MINB 4
+#ifndef RL_P1_CTAS
+#define RL_P1_CTAS 6  // resident CTAs per SM the register budget of phase 1 targets
 #endif
-#ifndef RL_P2_MINB
-#define RL_P2_MINB 4
+#ifndef RL_P2_CTAS
+#define RL_P2_CTAS 4
 #endif
 template <class T>
-__global__ void __launch_bounds__(256, RL_P1_MINB) k_cast_defer_p1(
+__global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
     CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
     T* __restrict__ out, uint32_t n, WalkRecord* __restrict__ q, unsigned* __restrict__ qn) {
   // queue layout: window records grow up from q[0], near-field records down
@@ -571,8 +429,8 @@ __global__ void __launch_bounds__(256, RL_P1_MINB) k_cast_defer_p1(
       base_s[threadIdx.x] = tot ? atomicAdd(qn + threadIdx.x, tot) : 0u;
     }
     __syncthreads();
-    const unsigned below = (1u << lane) - 1;
-    if (defer) {  // records are touched twice: stream them past L2 (evict-first)
+    if (defer) {
+      const unsigned below = (1u << lane) - 1;
       const size_t slot = win ? base_s[0] + cnt_s[0][wid] + __popc(bw & below)
                               : n - 1 - (base_s[1] + cnt_s[1][wid] + __popc(bn & below));
       const float4* src = reinterpret_cast<const float4*>(&rec);
@@ -587,9 +445,10 @@ __global__ void __launch_bounds__(256, RL_P1_MINB) k_cast_defer_p1(
 // NEAR: records whose origin needs the near-field walk, redone in full;
 // otherwise the pending verification windows, resumed in place.
 template <class T, bool NEAR>
-__global__ void __launch_bounds__(256, RL_P2_MINB) k_cast_defer_p2(
-    CddtView c, const WalkRecord* __restrict__ q, const unsigned* __restrict__ qn, uint32_t n,
-    T* __restrict__ out) {
+__global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_defer_p2(CddtView c,
+                                                          const WalkRecord* __restrict__ q,
+                                                          const unsigned* __restrict__ qn,
+                                                          uint32_t n, T* __restrict__ out) {
   const unsigned m = qn[NEAR ? 1 : 0];
   for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
     WalkRecord r;
@@ -612,137 +471,46 @@ __global__ void __launch_bounds__(256, RL_P2_MINB) k_cast_defer_p2(
   }
 }
 
-// One full wave: every SM holds as many 256-thread CTAs as registers allow
-// and the grid-stride loop spreads the queries evenly (no partial last wave).
+// CTAs per SM for a kernel at 256 threads (one full wave, no partial tail).
+template <class K>
+static int resident_ctas(K kernel) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  return std::max(per_sm, 1);
+}
+
 template <class T, class I, bool HIT, bool RES>
 static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t, T* out,
                           int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
-  static int per_sm = RL_GRID_PER_SM;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast<T, I, HIT, RES>, 256, 0);
-    if (per_sm <= 0) per_sm = 1;
-  }
+  static const int per_sm = resident_ctas(k_cast<T, I, HIT, RES>);
   const size_t b = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * per_sm));
-#if RL_L2_PERSIST
-  // keep the zero points L2-resident against the streaming query traffic
-  static size_t persist_max = 0;
-  if (!persist_max) {
-    int dev = 0, mx = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    persist_max = size_t(mx > 0 ? mx : 1);
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_max);
-  }
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-  const size_t zb = v.zp_bytes;
-  attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(v.zp);
-  attr[0].val.accessPolicyWindow.num_bytes = zb;
-  attr[0].val.accessPolicyWindow.hitRatio =
-      zb > persist_max ? float(double(persist_max) / double(zb)) : 1.0f;
-  attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(b));
-  cfg.blockDim = dim3(256);
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_cast<T, I, HIT, RES>, v, x, y, t, out, hit, rr, ri, I(n));
-#else
   k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
-#endif
 }
 
-#ifndef RL_CAST_SM
-#define RL_CAST_SM 0
-#endif
-// K3 (state-machine form, cddt_cast_sm.cuh)
-template <class T, bool HIT, bool RES>
-__global__ void __launch_bounds__(256, RL_CAST_MINB) k_cast_sm(
-    CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
-    T* __restrict__ out, int32_t* __restrict__ hit, int64_t* __restrict__ res_row,
-    int32_t* __restrict__ res_idx, size_t n) {
-  cast_stream<T, HIT, RES>(c, qx, qy, qt, out, hit, res_row, res_idx,
-                           blockIdx.x * size_t(blockDim.x) + threadIdx.x,
-                           size_t(gridDim.x) * blockDim.x, n);
-}
-
-template <class T, bool HIT, bool RES>
-static int sm_blocks(size_t n) {
-  static int per_sm = RL_GRID_PER_SM;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast_sm<T, HIT, RES>, 256, 0);
-    if (per_sm <= 0) per_sm = 1;
-  }
-  size_t b = (n + 255) / 256;
-  return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * per_sm)));
-}
+constexpr size_t kDeferMinQueries = size_t(1) << 22;
 
 // Dispatch of the batched cast kernels for the device-pointer entry points.
 template <class T>
-static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out, int32_t* hit,
-                        int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
-#if RL_CAST_SM
-  const CddtView v = c->view();
-  if (rr || ri) {
-    k_cast_sm<T, true, true><<<sm_blocks<T, true, true>(n), 256, 0, st>>>(v, x, y, t, out, hit,
-                                                                         rr, ri, n);
-  } else if (hit) {
-    k_cast_sm<T, true, false><<<sm_blocks<T, true, false>(n), 256, 0, st>>>(v, x, y, t, out, hit,
-                                                                           rr, ri, n);
-  } else {
-    k_cast_sm<T, false, false><<<sm_blocks<T, false, false>(n), 256, 0, st>>>(v, x, y, t, out,
-                                                                             hit, rr, ri, n);
-  }
-#else
+static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out,
+                       int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
-#if RL_DEFER_WALK
-  // small batches (a few waves) gain nothing from the split and pay two more launches
-  if (!rr && !ri && !hit && small && n >= (size_t(1) << 22)) {
+  if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
     rl_cddt* cm = const_cast<rl_cddt*>(c);
     const size_t need = sizeof(WalkRecord) * n + 256;
-    if (cm->defer_ws.n < need) cm->defer_ws.alloc(need);
+    if (cm->defer_ws.n < need) RL_TRY(cm->defer_ws.alloc(need));
     unsigned* qn = reinterpret_cast<unsigned*>(cm->defer_ws.p);
     WalkRecord* q = reinterpret_cast<WalkRecord*>(cm->defer_ws.p + 256);
-    cudaMemsetAsync(qn, 0, 2 * sizeof(unsigned), st);
-    static int p1 = 0, p2 = 0, p3 = 0;
-    if (!p1) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_cast_defer_p1<T>, 256, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_cast_defer_p2<T, false>, 256, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p3, k_cast_defer_p2<T, true>, 256, 0);
-      p1 = std::max(p1, 1);
-      p2 = std::max(p2, 1);
-      p3 = std::max(p3, 1);
-    }
+    static const int p1 = resident_ctas(k_cast_defer_p1<T>);
+    static const int p2 = resident_ctas(k_cast_defer_p2<T, false>);
+    static const int p3 = resident_ctas(k_cast_defer_p2<T, true>);
+    RL_CK(cudaMemsetAsync(qn, 0, 2 * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
     k_cast_defer_p2<T, false><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
     k_cast_defer_p2<T, true><<<sm_count() * p3, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
-    return;
+    return RL_OK;
   }
-#elif RL_TWO_PHASE
-  if (!rr && !ri && !hit && small) {
-    rl_cddt* cm = const_cast<rl_cddt*>(c);
-    const size_t need = sizeof(DeferredQuery) * n + 256;
-    if (cm->defer_ws.n < need) cm->defer_ws.alloc(need);
-    unsigned* qn = reinterpret_cast<unsigned*>(cm->defer_ws.p);
-    DeferredQuery* q = reinterpret_cast<DeferredQuery*>(cm->defer_ws.p + 256);
-    cudaMemsetAsync(qn, 0, sizeof(unsigned), st);
-    static int p1 = 0, p2 = 0;
-    if (!p1) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, k_cast_p1<T>, 256, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, k_cast_p2<T>, 256, 0);
-      p1 = std::max(p1, 1);
-      p2 = std::max(p2, 1);
-    }
-    const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
-    k_cast_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_cast_p2<T><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, out);
-    return;
-  }
-#endif
   if (rr || ri) {
     launch_k_cast<T, size_t, true, true>(v, x, y, t, out, hit, rr, ri, n, st);
   } else if (hit) {
@@ -756,7 +524,7 @@ static void launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T*
     else
       launch_k_cast<T, size_t, false, false>(v, x, y, t, out, hit, rr, ri, n, st);
   }
-#endif
+  return RL_OK;
 }
 
 __global__ void k_directional(CddtView c, const double* __restrict__ x,
@@ -868,8 +636,6 @@ int prune_structure(rl_cddt* c) {
   c->row_off = std::move(noff);
   c->zero_points = kept;
   c->pruned = true;
-  RL_TRY(refresh_guide(c));
-  RL_CK(cudaStreamSynchronize(st));
   return RL_OK;
 }
 
@@ -956,11 +722,9 @@ int rl_cddt_destroy(rl_cddt* c) {
     DeviceGuard guard(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     c->flags.release();
-    c->tiles.release();
     c->rowbits.release();
     c->row_off.release();
     c->zp.release();
-    c->zs.release();
     c->d_slices.release();
     c->d_dirs.release();
     c->d_scalar.release();
@@ -1038,7 +802,7 @@ int rl_cddt_cast_batch(rl_cddt* c, const float* x, const float* y, const float* 
   if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  launch_cast<float>(c, x, y, theta, out, hit, nullptr, nullptr, n, pick_stream(c, stream));
+  RL_TRY(launch_cast<float>(c, x, y, theta, out, hit, nullptr, nullptr, n, pick_stream(c, stream)));
   return finish(c, stream);
 }
 
@@ -1048,7 +812,8 @@ int rl_cddt_cast_batch_f64(rl_cddt* c, const double* x, const double* y, const d
   if (!c || (n && (!x || !y || !theta))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  launch_cast<double>(c, x, y, theta, out, hit, res_row, res_idx, n, pick_stream(c, stream));
+  RL_TRY(launch_cast<double>(c, x, y, theta, out, hit, res_row, res_idx, n,
+                             pick_stream(c, stream)));
   return finish(c, stream);
 }
 
@@ -1105,7 +870,7 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
     RL_CK(cudaMemcpyAsync(dx, x + off, m * 4, cudaMemcpyHostToDevice, l.s));
     RL_CK(cudaMemcpyAsync(dy, y + off, m * 4, cudaMemcpyHostToDevice, l.s));
     RL_CK(cudaMemcpyAsync(dt, theta + off, m * 4, cudaMemcpyHostToDevice, l.s));
-    launch_cast<float>(c, dx, dy, dt, dout, nullptr, nullptr, nullptr, m, l.s);
+    RL_TRY(launch_cast<float>(c, dx, dy, dt, dout, nullptr, nullptr, nullptr, m, l.s));
     RL_CK(cudaGetLastError());
     RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
   }

@@ -111,13 +111,10 @@ struct rl_cddt {
   std::vector<uint8_t> member_h;  // host mirror: membership
 
   rl::DevBuf<uint8_t> flags;        // w*h
-  rl::DevBuf<ulonglong2> tiles;     // 8x8 occupancy/clear tiles for queries
-  int tw = 0, th = 0;
   rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
   int wpr = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
   rl::DevBuf<float> zp;             // capacity >= zero_points
-  rl::DevBuf<float> zs;             // search guide zs[j] = zp[16 j]
   rl::DevBuf<rl::SliceParam> d_slices;
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
@@ -130,13 +127,10 @@ struct rl_cddt {
   rl::CddtView view() const {
     rl::CddtView v;
     v.flags = flags.p;
-    v.tiles = tiles.p;
-    v.tw = tw;
     v.rowbits = rowbits.p;
     v.wpr = wpr;
     v.row_off = row_off.p;
     v.zp = zp.p;
-    v.zs = zs.p;
     v.slices = d_slices.p;
     v.dirs = d_dirs.p;
     v.w = w;
@@ -144,7 +138,6 @@ struct rl_cddt {
     v.K = K;
     v.S = S;
     v.max_range = max_range;
-    v.zp_bytes = size_t(zero_points) * sizeof(float);
     return v;
   }
 };
@@ -155,6 +148,5 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
   return s ? static_cast<cudaStream_t>(s) : c->stream;
 }
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
-int refresh_tiles(rl_cddt* c);          // rebuild query tiles from flags
-int refresh_guide(rl_cddt* c);          // rebuild the search guide from zp
+int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 }  // namespace rl

@@ -25,7 +25,7 @@
 
 namespace rl {
 
-// same as in rl_cddt.cu (kept local: device code is per-TU)
+// for_each_bin_of_pixel (cddt.cpp:118-134), as in rl_cddt.cu (device code is per-TU)
 __device__ __forceinline__ void pixel_rows_u(const SliceParam& sp, int px, int py, int& r0,
                                              int& r1, float& v) {
   auto py_of = [&](double x, double y) { return -x * sp.sin_t + y * sp.cos_t + sp.y_offset; };
@@ -262,7 +262,7 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   RL_CK(cudaMemcpyAsync(d_wflags, wflags.data(), nw, cudaMemcpyHostToDevice, st));
   k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(d_wcells, d_wflags, int(nw), c->flags.p);
   RL_CK(cudaGetLastError());
-  RL_TRY(refresh_tiles(c));
+  RL_TRY(refresh_query_bits(c));
   if (nd == 0) return finish(c, nullptr);
 
   // 3. delta records; unused key slots stay at UINT64_MAX and sort last, so
@@ -301,7 +301,6 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   std::swap(c->zp, c->zp_spare);
   std::swap(c->row_off, c->off_spare);
   c->zero_points = total_miss[0];
-  RL_TRY(refresh_guide(c));
   return finish(c, nullptr);
 }
 
