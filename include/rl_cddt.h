@@ -126,6 +126,22 @@ int rl_cddt_export(const rl_cddt *c, uint32_t *slice_row_base, uint64_t *row_off
 int rl_cddt_serialize(const rl_cddt *c, uint8_t *buf, size_t cap, size_t *size);
 int rl_cddt_deserialize(const uint8_t *buf, size_t n, int32_t device, rl_cddt **out);
 
+/* oracle_cast (proj/src/raycast.cpp:9-16) on the handle's grid: the exact
+ * distance to the first occupied cell along a continuous direction, clamped
+ * to max_range. Device pointers. cos_t/sin_t (optional, both or neither) give
+ * the direction per query — pass glibc cos/sin of the normalised angle for
+ * bit parity with the reference; with NULL the device computes sincos(theta)
+ * (within 1 ulp of glibc). */
+int rl_exact_cast_batch(rl_cddt *c, const double *x, const double *y, const double *theta,
+                        const double *cos_t, const double *sin_t, double *out, size_t n,
+                        void *stream);
+
+/* lut_build (proj/src/raycast.cpp:62-87) on the handle's grid and max_range:
+ * entries[(i * height + y) * width + x] = clamp(llround(oracle_cast(x + 0.5,
+ * y + 0.5, i * 2pi / theta_disc)), 0, 65535), written to device memory
+ * (2 * width * height * theta_disc bytes). */
+int rl_lut_build(rl_cddt *c, int32_t theta_disc, uint16_t *entries, void *stream);
+
 /* Wait for all work queued on the handle's stream. */
 int rl_cddt_sync(rl_cddt *c);
 

@@ -108,6 +108,8 @@ def ref_lib() -> C.CDLL:
         h.ref_beam_likelihood.argtypes = [_P, _d, _d]
         h.ref_beam_likelihood.restype = _d
         h.ref_sensor_update.argtypes = [_P, _P, _P, _P, C.c_long, _P, C.c_int, _d, _P, _P, C.c_int]
+        h.ref_oracle_batch.argtypes = [_P, _P, _P, _P, _sz, _P]
+        h.ref_lut_build.argtypes = [_P, C.c_int, _P]
         h.ref_rm_create.argtypes = [_P, _i32, _i32, _d]
         h.ref_rm_create.restype = _P
         h.ref_rm_destroy.argtypes = [_P]
@@ -308,6 +310,19 @@ class RefCddt(_Base):
         ref_lib().ref_cast_pair_batch(self._h, x.ctypes.data, y.ctypes.data, t.ctypes.data,
                                       x.size, f.ctypes.data, b.ctypes.data)
         return f, b
+
+    def oracle_batch(self, x, y, t):
+        x, y, t = _a(x, np.float64), _a(y, np.float64), _a(t, np.float64)
+        out = np.empty(x.size)
+        ref_lib().ref_oracle_batch(self._h, x.ctypes.data, y.ctypes.data, t.ctypes.data, x.size,
+                                   out.ctypes.data)
+        return out
+
+    def lut_build(self, theta_disc):
+        i = self.info()
+        out = np.empty((theta_disc, i["height"], i["width"]), np.uint16)
+        assert ref_lib().ref_lut_build(self._h, theta_disc, out.ctypes.data) == 0
+        return out
 
     def sensor_update(self, px, py, pt, scan, fov, params, paired=False):
         px, py, pt, scan = (_a(v, np.float64) for v in (px, py, pt, scan))

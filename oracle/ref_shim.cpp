@@ -276,6 +276,28 @@ int ref_sensor_update(void* hp, const double* px, const double* py, const double
   return ok ? 0 : 1;
 }
 
+// oracle_cast (proj/src/raycast.cpp:9-16) and lut_build (:62-87) on the
+// structure's grid and max_range.
+void ref_oracle_batch(void* hp, const double* x, const double* y, const double* t, size_t n,
+                      double* out) {
+  const RefCddt& r = *static_cast<RefCddt*>(hp);
+  for (size_t i = 0; i < n; i++)
+    out[i] = oracle_cast(r.c.grid(), RayQuery(x[i], y[i], t[i]), r.c.max_range());
+}
+int ref_lut_build(void* hp, int theta_disc, uint16_t* out) {
+  const RefCddt& r = *static_cast<RefCddt*>(hp);
+  try {
+    RangeMethodConfig cfg;
+    cfg.max_range = r.c.max_range();
+    cfg.theta_disc = theta_disc;
+    LookupTable lut = lut_build(r.c.grid(), cfg, size_t(1) << 34);
+    std::memcpy(out, lut.entries.data(), lut.entries.size() * sizeof(uint16_t));
+    return RS_OK;
+  } catch (...) {
+    return RS_EOTHER;
+  }
+}
+
 // Ray marching baseline (make_method(ray_march), proj/src/methods.cpp:55-72).
 void* ref_rm_create(const uint8_t* grid, int w, int h, double max_range) {
   try {

@@ -341,6 +341,24 @@ class Cddt:
                                               x.numel(), s))
         return out
 
+    def exact_cast_batch(self, x, y, theta=None, cos_t=None, sin_t=None, out=None, stream=None):
+        """oracle_cast (raycast.cpp:9-16) on this structure's grid (torch CUDA f64)."""
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        s = stream if stream is not None else _cur_stream(x)
+        check(lib().rl_exact_cast_batch(self._h, _ptr(x), _ptr(y), _ptr(theta), _ptr(cos_t),
+                                        _ptr(sin_t), _ptr(out), x.numel(), s))
+        return out
+
+    def lut_build(self, theta_disc: int):
+        """lut_build (raycast.cpp:62-87) on the GPU: uint16 [theta_disc, h, w] (torch CUDA)."""
+        import torch
+        i = self._info
+        e = torch.empty((theta_disc, i.height, i.width), dtype=torch.int16, device=f"cuda:{i.device}")
+        check(lib().rl_lut_build(self._h, theta_disc, e.data_ptr(), _cur_stream(e)))
+        return e
+
     # ---- structure maintenance ----
     def prune(self) -> None:
         check(lib().rl_cddt_prune(self._h))

@@ -411,3 +411,43 @@ def test_full_size_edit_rounds_vs_reference_hashes(rl, synth):
         assert _sha(e["zp"]) == rd["zp_sha"]
         assert _sha(e["row_off"]) == rd["row_off_sha"]
         assert _sha(e["membership"]) == rd["membership_sha"]
+
+
+# ---- oracle_cast and lut_build on the GPU ----
+def test_exact_cast_vs_reference_oracle(rl, oracle_mod, synth):
+    import math
+    import torch
+    if not oracle_mod.ref_available():
+        pytest.skip("reference not compiled")
+    g = synth.rect_map(120, 90, 8, seed=5)
+    gpu = make_gpu(rl, g, 36, 60.0)
+    ref = oracle_mod.RefCddt(g, 36, 60.0)
+    rng = np.random.default_rng(11)
+    n = 20000
+    x, y = rng.uniform(-2, 122, n), rng.uniform(-2, 92, n)
+    t = rng.uniform(-7, 13, n)
+    # glibc cos/sin of the normalised angle (what RayQuery + oracle_cast use)
+    tn = np.array([rl.normalize_angle_2pi(v) for v in t])
+    cs = np.array([math.cos(v) for v in tn])
+    sn = np.array([math.sin(v) for v in tn])
+    want = ref.oracle_batch(x, y, t)
+    got = gpu.exact_cast_batch(dev(x), dev(y), dev(t), dev(cs), dev(sn))
+    approx = gpu.exact_cast_batch(dev(x), dev(y), dev(t))
+    torch.cuda.synchronize()
+    assert np.array_equal(host(got).view(np.uint64), want.view(np.uint64))
+    # device sincos: within the north-star range tolerance
+    d = np.abs(host(approx) - want)
+    assert np.all((d <= 1e-3) | (d <= 1e-4 * np.abs(want)))
+
+
+def test_lut_build_vs_reference(rl, oracle_mod, synth):
+    import torch
+    if not oracle_mod.ref_available():
+        pytest.skip("reference not compiled")
+    g = synth.rect_map(64, 48, 5, seed=9)
+    for K, mr in ((16, 0.0), (36, 25.0)):
+        gpu = make_gpu(rl, g, 36, mr)
+        ref = oracle_mod.RefCddt(g, 36, mr)
+        got = gpu.lut_build(K)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(got).view(np.uint16), ref.lut_build(K))
