@@ -110,6 +110,7 @@ def ref_lib() -> C.CDLL:
         h.ref_sensor_update.argtypes = [_P, _P, _P, _P, C.c_long, _P, C.c_int, _d, _P, _P, C.c_int]
         h.ref_oracle_batch.argtypes = [_P, _P, _P, _P, _sz, _P]
         h.ref_lut_build.argtypes = [_P, C.c_int, _P]
+        h.ref_bench.argtypes = [_P, C.c_int, _sz, C.c_uint64, C.c_int, _P, C.c_char_p]
         h.ref_rm_create.argtypes = [_P, _i32, _i32, _d]
         h.ref_rm_create.restype = _P
         h.ref_rm_destroy.argtypes = [_P]
@@ -317,6 +318,13 @@ class RefCddt(_Base):
         ref_lib().ref_oracle_batch(self._h, x.ctypes.data, y.ctypes.data, t.ctypes.data, x.size,
                                    out.ctypes.data)
         return out
+
+    def bench(self, random_mode: bool, n: int = 0, seed: int = 1, stride: int = 4):
+        """The reference's run_random/grid_benchmark: (queries, checksum, map_id)."""
+        out = np.zeros(2)
+        mid = C.create_string_buffer(17)
+        ref_lib().ref_bench(self._h, 1 if random_mode else 0, n, seed, stride, out.ctypes.data, mid)
+        return int(out[0]), float(out[1]), mid.value.decode()
 
     def lut_build(self, theta_disc):
         i = self.info()

@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "rangelib/bench.hpp"
 #include "rangelib/cddt.hpp"
 #include "rangelib/grid.hpp"
 #include "rangelib/mcl.hpp"
@@ -296,6 +297,22 @@ int ref_lut_build(void* hp, int theta_disc, uint16_t* out) {
   } catch (...) {
     return RS_EOTHER;
   }
+}
+
+// run_random_benchmark / run_grid_benchmark (proj/src/bench.cpp:153-210) over
+// the Cddt: out = {queries, checksum}; map_content_id into id (17 bytes).
+void ref_bench(void* hp, int random_mode, size_t n, uint64_t seed, int stride, double* out,
+               char* id) {
+  const RefCddt& r = *static_cast<RefCddt*>(hp);
+  CddtView view(r.c, true);
+  RangeMethodConfig cfg;
+  cfg.max_range = r.c.max_range();
+  cfg.theta_disc = r.c.theta_disc();
+  BenchReport rep = random_mode ? run_random_benchmark(view, r.c.grid(), cfg, n, seed)
+                                : run_grid_benchmark(view, r.c.grid(), cfg, stride);
+  out[0] = double(rep.queries);
+  out[1] = rep.checksum;
+  std::strncpy(id, rep.map_id.c_str(), 17);
 }
 
 // Ray marching baseline (make_method(ray_march), proj/src/methods.cpp:55-72).

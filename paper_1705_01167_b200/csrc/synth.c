@@ -403,3 +403,14 @@ int synth_trajectory(const uint8_t *g, int w, int h, double x, double y, double 
   }
   return 0;
 }
+
+/* FNV-1a 64 over the width, height (little-endian bytes) and 0/1 cell
+ * stream: the reference's map_content_id (proj/src/bench.cpp:22-34). */
+uint64_t synth_map_fnv1a(const uint8_t *g, int w, int h) {
+  uint64_t x = 1469598103934665603ull;
+  for (int shift = 0; shift < 32; shift += 8) x = (x ^ ((uint32_t)w >> shift & 0xff)) * 1099511628211ull;
+  for (int shift = 0; shift < 32; shift += 8) x = (x ^ ((uint32_t)h >> shift & 0xff)) * 1099511628211ull;
+  size_t n = (size_t)w * h;
+  for (size_t i = 0; i < n; i++) x = (x ^ (uint64_t)(g[i] ? 1 : 0)) * 1099511628211ull;
+  return x;
+}

@@ -36,6 +36,8 @@ def lib() -> C.CDLL:
         h.synth_particles.argtypes = [d, d, d, d, d, u64, C.c_long, P, P, P]
         h.synth_scan.argtypes = [P, i32, i32, d, d, d, i32, d, d, d, d, u64, P]
         h.synth_trajectory.argtypes = [P, i32, i32, d, d, d, C.c_long, d, d, u64, P, P]
+        h.synth_map_fnv1a.argtypes = [P, i32, i32]
+        h.synth_map_fnv1a.restype = u64
         _lib = h
     return _lib
 
@@ -63,6 +65,12 @@ def free_queries_gpu(grid_dev, w: int, h: int, n: int, seed=7, start=0, out=None
     assert _gpu.synth_free_queries_gpu(grid_dev.data_ptr(), w, h, seed, start, n, qx.data_ptr(),
                                        qy.data_ptr(), qt.data_ptr(), stream) == 0
     return qx, qy, qt
+
+
+def map_fnv1a(grid) -> int:
+    """map_content_id's hash (proj/src/bench.cpp:22-34) of a uint8 [h, w] grid."""
+    g = np.ascontiguousarray(grid, dtype=np.uint8)
+    return int(lib().synth_map_fnv1a(g.ctypes.data, g.shape[1], g.shape[0]))
 
 
 def rect_map(w=500, h=500, nrect=40, seed=2) -> np.ndarray:
