@@ -157,8 +157,9 @@ def run_bench(method: rl.CddtMethod, grid, cfg, x, y, t, mode: str, seed: int,
                 memory_bytes=method.memory_bytes(), speedup_vs_bl=None, histogram=hist)
 
 
-def emit(reports: list[dict], fmt: str, out=sys.stdout) -> None:
+def emit(reports: list[dict], fmt: str, out=None) -> None:
     """report_emit (bench.cpp:235-317)."""
+    out = out or sys.stdout
     if fmt == "jsonl":
         for r in reports:
             out.write(json.dumps(r) + "\n")
