@@ -451,3 +451,50 @@ def test_lut_build_vs_reference(rl, oracle_mod, synth):
         got = gpu.lut_build(K)
         torch.cuda.synchronize()
         assert np.array_equal(host(got).view(np.uint16), ref.lut_build(K))
+
+
+# ---- the deferred-walk batch path (f32, >= 4M queries) ----
+def _deferred_vs_oracle(rl, oracle_mod, g, K, mr, qx, qy, qt):
+    import torch
+    assert qx.size >= (1 << 22)  # large enough for the split kernels
+    gpu = make_gpu(rl, g, K, mr)
+    got = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
+    torch.cuda.synchronize()
+    want = oracle_mod.OracleCddt(g, K, mr).cast_batch(qx, qy, qt, want_f64=False, want_hit=False,
+                                                      want_res=False)["out32"]
+    bad = np.flatnonzero(host(got).view(np.uint32) != want.view(np.uint32))
+    assert bad.size == 0, (bad[:10], host(got)[bad[:10]], want[bad[:10]])
+
+
+def test_deferred_path_maze(rl, oracle_mod, synth):
+    g = synth.maze_map(1000, 1000, 0.10, 8)
+    qx, qy, qt = synth.free_queries(g, 5_000_000, seed=3)
+    _deferred_vs_oracle(rl, oracle_mod, g, 120, 500.0, qx, qy, qt)
+
+
+def test_deferred_path_edge_cases(rl, oracle_mod):
+    """Origins anywhere (off-map, occupied, next to walls), a tiny max_range
+    (below the near field and the verification window), theta_disc 4, angles
+    far outside [0, 2pi)."""
+    rng = np.random.default_rng(5)
+    g = (rng.random((61, 83)) < 0.25).astype(np.uint8)
+    n = 1 << 22
+    qx = rng.uniform(-3, 86, n).astype(np.float32)
+    qy = rng.uniform(-3, 64, n).astype(np.float32)
+    qt = rng.uniform(-40, 40, n).astype(np.float32)
+    qx[: n // 8] = np.round(qx[: n // 8])  # exactly on lattice lines
+    for K, mr in ((4, 0.0), (24, 0.5), (216, 2.0)):
+        _deferred_vs_oracle(rl, oracle_mod, g, K, mr, qx, qy, qt)
+
+
+def test_deferred_path_equals_single_kernel_cfg3(rl, synth):
+    """Config-3 PCDDT: the split f32 batch equals float() of the single-kernel
+    f64 batch on 8M queries."""
+    import torch
+    g = synth.polygon_map()
+    gpu = make_gpu(rl, g, 200, 1000.0, prune=True)
+    qx, qy, qt = synth.free_queries(g, 8_000_000, seed=77)
+    split = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
+    whole = gpu.cast_batch_f64(*(dev(a.astype(np.float64)) for a in (qx, qy, qt)))
+    torch.cuda.synchronize()
+    assert torch.equal(split, whole.float())
