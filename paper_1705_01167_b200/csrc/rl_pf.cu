@@ -114,14 +114,17 @@ __global__ void __launch_bounds__(kMomentBlock) k_weights(
   }
 }
 
+// one warp per moment: lane-strided partial sums, then a fixed shuffle tree
+// (deterministic for a given block count)
 __global__ void k_sum_partials(const double* __restrict__ partial, int nblk,
                                double* __restrict__ moments) {
-  const int k = threadIdx.x;
-  if (k < 10) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; b++) s += partial[b * 10 + k];
-    moments[k] = s;
-  }
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (k >= 10) return;
+  double s = 0.0;
+  for (int b = lane; b < nblk; b += 32) s += partial[b * 10 + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) moments[k] = s;
 }
 
 __global__ void k_normalize(double* __restrict__ w, size_t n, const double* __restrict__ moments,
@@ -183,7 +186,7 @@ int weights_launch(const double* logw, const double* gmax, const double* x, cons
                    cudaStream_t st) {
   const int nb = blocks(n, kMomentBlock, 2);
   k_weights<<<nb, kMomentBlock, 0, st>>>(logw, gmax, x, y, t, n, w, partial);
-  k_sum_partials<<<1, 32, 0, st>>>(partial, nb, moments);
+  k_sum_partials<<<1, 320, 0, st>>>(partial, nb, moments);
   RL_CK(cudaGetLastError());
   return RL_OK;
 }
