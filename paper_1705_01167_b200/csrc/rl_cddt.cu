@@ -496,11 +496,24 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
   if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
-    rl_cddt* cm = const_cast<rl_cddt*>(c);
-    const size_t need = sizeof(WalkRecord) * n + 256;
-    if (cm->defer_ws.n < need) RL_TRY(cm->defer_ws.alloc(need));
-    unsigned* qn = reinterpret_cast<unsigned*>(cm->defer_ws.p);
-    WalkRecord* q = reinterpret_cast<WalkRecord*>(cm->defer_ws.p + 256);
+    // stream-ordered scratch: concurrent batches on other streams (e.g. the
+    // pipelined host path) each get their own queue; the pool keeps the
+    // memory reserved, so steady-state allocation is free
+    static const bool pool_ready = [] {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      return true;
+    }();
+    (void)pool_ready;
+    uint8_t* ws = nullptr;
+    RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(WalkRecord) * n + 256, st));
+    unsigned* qn = reinterpret_cast<unsigned*>(ws);
+    WalkRecord* q = reinterpret_cast<WalkRecord*>(ws + 256);
     static const int p1 = resident_ctas(k_cast_defer_p1<T>);
     static const int p2 = resident_ctas(k_cast_defer_p2<T, false>);
     static const int p3 = resident_ctas(k_cast_defer_p2<T, true>);
@@ -509,6 +522,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
     k_cast_defer_p2<T, false><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
     k_cast_defer_p2<T, true><<<sm_count() * p3, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+    RL_CK(cudaFreeAsync(ws, st));
     return RL_OK;
   }
   if (rr || ri) {
@@ -729,7 +743,6 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->d_dirs.release();
     c->d_scalar.release();
     c->ws.release();
-    c->defer_ws.release();
     c->upd_ws.release();
     c->zp_spare.release();
     c->off_spare.release();

@@ -119,7 +119,6 @@ struct rl_cddt {
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
-  rl::DevBuf<uint8_t> defer_ws;     // two-phase cast: deferred-query records
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off

@@ -498,3 +498,25 @@ def test_deferred_path_equals_single_kernel_cfg3(rl, synth):
     whole = gpu.cast_batch_f64(*(dev(a.astype(np.float64)) for a in (qx, qy, qt)))
     torch.cuda.synchronize()
     assert torch.equal(split, whole.float())
+
+
+def test_concurrent_batches_on_two_streams(rl, synth):
+    """Two large batches on different streams against one handle (the pattern of
+    the pipelined host path) give the same results as one after the other."""
+    import torch
+    g = synth.maze_map(800, 800, 0.1, 2)
+    gpu = make_gpu(rl, g, 120, 300.0)
+    a = [dev(v) for v in synth.free_queries(g, 5_000_000, seed=1)]
+    b = [dev(v) for v in synth.free_queries(g, 5_000_000, seed=2)]
+    ra = gpu.cast_batch(*a)
+    rb = gpu.cast_batch(*b)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    oa, ob = torch.empty_like(ra), torch.empty_like(rb)
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            gpu.cast_batch(*a, out=oa)
+        with torch.cuda.stream(s2):
+            gpu.cast_batch(*b, out=ob)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ra) and torch.equal(ob, rb)
