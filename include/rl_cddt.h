@@ -20,6 +20,11 @@
  *    pointers and return when the results are in host memory.
  *  - Status codes mirror the reference's exceptions; the message of the last
  *    failure on the calling thread is available from rl_last_error().
+ *  - Threading follows the reference's single-writer / many-reader contract
+ *    (SPEC.md:341): casts (single, batched, from any thread or stream) may run
+ *    concurrently on one handle; prune, set_occupancy* and deserialize-style
+ *    structure changes need exclusive access; sensor/particle-filter calls on
+ *    one handle are serialised internally.
  */
 #ifndef RL_CDDT_H
 #define RL_CDDT_H

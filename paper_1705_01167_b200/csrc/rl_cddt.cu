@@ -787,6 +787,7 @@ int rl_cddt_sync(rl_cddt* c) {
 
 static int single(rl_cddt* c, double x, double y, double theta, int pair, double* o0,
                   double* o1) {
+  std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   if (!c->d_scalar.p) RL_TRY(c->d_scalar.alloc(2));
   k_single<<<1, 1, 0, c->stream>>>(c->view(), x, y, theta, pair, c->d_scalar.p);

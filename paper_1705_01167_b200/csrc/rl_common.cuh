@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -119,6 +120,7 @@ struct rl_cddt {
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
+  std::mutex mu;                    // serialises users of d_scalar / ws / the handle stream
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off

@@ -285,6 +285,7 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
                 uint64_t seed, uint64_t iteration, double* estimate, void* stream) {
   if (!c || !noise || !scan || nbeams <= 0 || (n && (!x || !y || !theta || !w))) return RL_EINVAL;
   if (n == 0) return RL_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
   // workspace: logw | w2 x y t (resample targets) | cdf | partials | moments | max | flag | cub

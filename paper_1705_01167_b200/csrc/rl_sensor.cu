@@ -217,6 +217,7 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
                      double inv_res, double* logw, double* weight, void* stream) {
   RL_TRY(check_sensor_args(c, px, py, pt, n, scan, nbeams, params, table, zdim, inv_res));
   if (n == 0) return RL_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
   // workspace: logw (if not given) | w (if not given) | max | sum | flag | cub temp
