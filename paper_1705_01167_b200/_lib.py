@@ -114,6 +114,19 @@ def lib() -> C.CDLL:
     return _lib
 
 
+# cudaStreamLegacy: the legacy default stream named explicitly. A NULL stream
+# means "the handle's own stream, synchronous" in the C ABI, so torch's
+# default stream (pointer 0) must be passed as this handle to keep the ops
+# ordered with torch's work.
+CUDA_STREAM_LEGACY = 1
+
+
+def torch_stream(device) -> C.c_void_p:
+    """The C-ABI stream argument for torch's current stream on `device`."""
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream or CUDA_STREAM_LEGACY)
+
+
 def check(status: int) -> int:
     """Map a status code to the reference's exception types."""
     if status in (RL_OK, RL_EDEGENERATE):

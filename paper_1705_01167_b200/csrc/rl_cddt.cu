@@ -746,6 +746,8 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->upd_ws.release();
     c->zp_spare.release();
     c->off_spare.release();
+    c->pf_ctl.release();
+    if (c->pf_host) cudaFreeHost(c->pf_host);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;

@@ -120,7 +120,10 @@ struct rl_cddt {
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
-  std::mutex mu;                    // serialises users of d_scalar / ws / the handle stream
+  std::mutex mu;                    // serialises users of d_scalar / ws / pf_* / the handle stream
+  rl::DevBuf<uint8_t> pf_ctl;       // fused PF step: {max key, ticket} | moments (zeroed when dirty)
+  bool pf_ctl_clean = false;        // the max key is 0 (every completed step leaves it so)
+  void* pf_host = nullptr;          // fused PF step: pinned host copy of the moments
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off

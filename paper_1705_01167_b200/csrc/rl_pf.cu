@@ -2,148 +2,202 @@
 // Mcl::estimate and resample_low_variance (proj/src/mcl.cpp:42-56, 108-142,
 // 176-201), plus the single-GPU fused Mcl::step.
 //
-// Randomness is counter-based (Philox4x32-10): particle i's motion noise at
-// iteration k is a pure function of (seed, i, k), so sharding particles over
-// GPUs does not change any draw. The reference's std::mt19937_64 +
-// std::normal_distribution stream is implementation-defined and cannot be
-// reproduced bit-for-bit; the restatement in oracle/cddt_oracle.c uses the
-// same Philox + Box-Muller and pins this path instead.
+// Randomness is counter-based (Philox4x32-10, pf_device.cuh): particle i's
+// motion noise at iteration k is a pure function of (seed, i, k), so sharding
+// particles over GPUs does not change any draw. The reference's
+// std::mt19937_64 + std::normal_distribution stream is implementation-defined
+// and cannot be reproduced bit-for-bit; the restatement in
+// oracle/cddt_oracle.c uses the same Philox + Box-Muller and pins this path
+// instead.
 //
-// Reductions are deterministic: per-block partials in a fixed-order second
-// pass (no floating-point atomics), and the cumulative weights come from a
-// CUB scan whose association depends only on n.
+// Reductions are deterministic (run to run and for a given n): per-block
+// partials summed in fixed order by the last block to finish (no
+// floating-point atomics), and the cumulative weights are a tiled scan —
+// fixed-shape block scans plus a sequential pass over tile totals — so the
+// comb sees the same cumulative sums on every run and on every rank.
+//
+// The fused step (rl_mcl_step) is two kernels:
+//   k_sensor_logw<true>  motion + casts + log-likelihood sums + atomic max
+//   k_pf_finish          one cooperative launch, phases split by grid syncs:
+//                        exp(logw - max) and moments | w / S tile scans |
+//                        tile prefix | low-variance comb | copy back
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 
+#include "pf_device.cuh"
 #include "rl_common.cuh"
 
 namespace rl {
 
-int sensor_logw_launch(rl_cddt* c, const double* px, const double* py, const double* pt,
-                       size_t n, const double* scan, int nb, double fov,
-                       const rl_beam_params_t* params, const float* table, int zdim,
-                       double inv_res, double* logw, cudaStream_t st);
+namespace cg = cooperative_groups;
 
-// Philox4x32-10 (Salmon et al., SC'11): counter (c0..c3), key (k0, k1).
-struct U4 {
-  uint32_t x, y, z, w;
-};
-__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; r++) {
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return c;
-}
-
-// two uniforms in [0, 1) with 53 random bits each
-__device__ __forceinline__ void philox_uniform2(uint64_t seed, uint32_t i, uint32_t draw,
-                                                uint64_t iter, double& u0, double& u1) {
-  const U4 r = philox4x32_10(U4{i, draw, uint32_t(iter), uint32_t(iter >> 32)}, uint32_t(seed),
-                             uint32_t(seed >> 32));
-  const uint64_t a = (uint64_t(r.y) << 32) | r.x, b = (uint64_t(r.w) << 32) | r.z;
-  u0 = double(a >> 11) * 0x1.0p-53;
-  u1 = double(b >> 11) * 0x1.0p-53;
-}
-
-constexpr uint32_t kResampleStream = 0xFFFFFFFFu;
+int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
+                       const double* scan, int nb, double fov, const rl_beam_params_t* params,
+                       const float* table, int zdim, double inv_res, double* logw,
+                       const MotionArgs* mot, unsigned long long* gmax_key, cudaStream_t st);
 
 __global__ void k_motion(double* __restrict__ x, double* __restrict__ y, double* __restrict__ t,
-                         size_t n, uint64_t off, double dx, double dy, double dth, double st,
-                         double sr, uint64_t seed, uint64_t iter) {
+                         size_t n, MotionArgs m) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t gi = uint32_t(off + i);
-    double a0, a1, b0, b1;
-    philox_uniform2(seed, gi, 0, iter, a0, a1);
-    philox_uniform2(seed, gi, 1, iter, b0, b1);
-    // Box-Muller on (0, 1] x [0, 1)
-    const double ra = sqrt(-2.0 * log(1.0 - a0)), rb = sqrt(-2.0 * log(1.0 - b0));
-    double sa, ca, sb, cb;
-    sincos(kTwoPi * a1, &sa, &ca);
-    sincos(kTwoPi * b1, &sb, &cb);
-    const double n0 = ra * ca, n1 = ra * sa, n2 = rb * cb;
-    (void)sb;
-    // motion_update (mcl.cpp:49-55)
-    const double rdx = dx + st * n0, rdy = dy + st * n1, rdt = dth + sr * n2;
-    double s, c;
-    sincos(t[i], &s, &c);
-    x[i] += rdx * c - rdy * s;
-    y[i] += rdx * s + rdy * c;
-    t[i] = normalize_angle_2pi(t[i] + rdt);
+    double xi = x[i], yi = y[i], ti = t[i];
+    motion_one(m, uint32_t(m.index_offset + i), xi, yi, ti);
+    x[i] = xi;
+    y[i] = yi;
+    t[i] = ti;
   }
 }
 
-// per-block partial moments, then a single-block fixed-order sum
-constexpr int kMomentBlock = 256;
-__global__ void __launch_bounds__(kMomentBlock) k_weights(
-    const double* __restrict__ logw, const double* __restrict__ gmax,
-    const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ t,
-    size_t n, double* __restrict__ w, double* __restrict__ partial) {
-  const double m = *gmax;
-  double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+// The sensor-model block of the step: moments[0..9] (see rl_pf_weights) and,
+// for the fused step, the degenerate flag of mcl.cpp:114-117.
+struct Moments {
+  double m[10];
+  int32_t degenerate;
+  int32_t pad;
+};
+
+constexpr int kPfThreads = 256;
+constexpr int kPfWarps = kPfThreads / 32;
+
+// ---- shared pieces: every path (fused step, stage entry points) runs the
+// same code with the same block count, so the sums are bit-identical ----
+
+// exp(logw - m) for this thread's grid-stride particles, accumulated moments
+__device__ __forceinline__ void weight_moments(const double* __restrict__ logw, double m,
+                                               const double* __restrict__ x,
+                                               const double* __restrict__ y,
+                                               const double* __restrict__ t, size_t n,
+                                               double* __restrict__ w, double acc[10]) {
+#pragma unroll
+  for (int k = 0; k < 10; k++) acc[k] = 0.0;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
     const double e = exp(logw[i] - m);
     w[i] = e;
     double s, c;
     sincos(t[i], &s, &c);
+    const double xi = x[i], yi = y[i];
     acc[0] += e;
-    acc[1] += e * x[i];
-    acc[2] += e * y[i];
+    acc[1] += e * xi;
+    acc[2] += e * yi;
     acc[3] += e * c;
     acc[4] += e * s;
     acc[5] += 1.0;
-    acc[6] += x[i];
-    acc[7] += y[i];
+    acc[6] += xi;
+    acc[7] += yi;
     acc[8] += c;
     acc[9] += s;
   }
-  typedef cub::BlockReduce<double, kMomentBlock> BR;
-  __shared__ typename BR::TempStorage tmp;
+}
+
+// block sum of the 10 accumulators (warp shuffle tree, then warps in order)
+// into partial[blockIdx.x * 10 + k]
+__device__ __forceinline__ void block_moments(double acc[10], double* __restrict__ partial) {
+  __shared__ double red[kPfWarps][10];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int k = 0; k < 10; k++) {
-    const double v = BR(tmp).Sum(acc[k]);
-    if (threadIdx.x == 0) partial[blockIdx.x * 10 + k] = v;
-    __syncthreads();
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    double v = 0.0;
+#pragma unroll
+    for (int wi = 0; wi < kPfWarps; wi++) v += red[wi][threadIdx.x];
+    partial[blockIdx.x * 10 + threadIdx.x] = v;
   }
 }
 
-// one warp per moment: lane-strided partial sums, then a fixed shuffle tree
-// (deterministic for a given block count)
-__global__ void k_sum_partials(const double* __restrict__ partial, int nblk,
-                               double* __restrict__ moments) {
-  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (k >= 10) return;
+// sum over the nblk partials of moment k by one warp: lane-strided sums,
+// then a fixed shuffle tree; lane 0 holds the result
+__device__ __forceinline__ double sum_partials(const double* __restrict__ partial, int nblk, int k) {
+  const int lane = threadIdx.x & 31;
   double s = 0.0;
-  for (int b = lane; b < nblk; b += 32) s += partial[b * 10 + k];
+#pragma unroll 4
+  for (int b = lane; b < nblk; b += 32) s += __ldcg(partial + b * 10 + k);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if (lane == 0) moments[k] = s;
+  return s;
 }
 
-__global__ void k_normalize(double* __restrict__ w, size_t n, const double* __restrict__ moments,
-                            uint64_t n_total, int32_t* __restrict__ degenerate) {
-  const double s = moments[0];
-  const bool bad = !(s > 0.0) || !isfinite(s);  // mcl.cpp:114-117
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x)
-    w[i] = bad ? 1.0 / double(n_total) : w[i] / s;
-  if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) *degenerate = bad ? 1 : 0;
+__device__ __forceinline__ bool degenerate_sum(double s) {
+  return !(s > 0.0) || !isfinite(s);  // mcl.cpp:114-117
 }
 
-// slot m takes the first particle i with cdf[i] >= r + m/n, capped at n-1
-// (the sequential comb of mcl.cpp:130-140)
-__global__ void k_comb(const double* __restrict__ cdf, const double* __restrict__ x,
-                       const double* __restrict__ y, const double* __restrict__ t, size_t n,
-                       size_t out_begin, size_t out_count, double* __restrict__ ox,
-                       double* __restrict__ oy, double* __restrict__ ot, double* __restrict__ ow,
-                       uint64_t seed, uint64_t iter) {
+// Tiled inclusive scan of the normalised weights. Tile j covers
+// [j*kScanTile, (j+1)*kScanTile); local[i] is the inclusive sum within the
+// tile and tile_excl[j] the sum of the earlier tile totals, so the cumulative
+// weight of particle i is tile_excl[i / kScanTile] + local[i]. With
+// normalise the input is w/S (or 1/n when S is degenerate) exactly as
+// k_normalize computes it.
+constexpr int kScanItems = 8, kScanTile = kPfThreads * kScanItems;
+
+struct ScanSmem {
+  typename cub::BlockScan<double, kPfThreads>::TempStorage scan;
+};
+
+__device__ __forceinline__ void scan_tile(const double* __restrict__ w, size_t n, size_t tile,
+                                          bool normalise, double s, bool bad,
+                                          double* __restrict__ local,
+                                          double* __restrict__ tile_total, ScanSmem& sm) {
+  const size_t base = tile * kScanTile + size_t(threadIdx.x) * kScanItems;
+  double v[kScanItems];
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++) {
+    const size_t i = base + k;
+    double a = 0.0;
+    if (i < n) {
+      const double wi = __ldcg(w + i);  // may come from another block of this grid
+      a = normalise ? (bad ? 1.0 / double(n) : wi / s) : wi;
+    }
+    v[k] = a;
+  }
+  double total;
+  cub::BlockScan<double, kPfThreads>(sm.scan).InclusiveSum(v, v, total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; k++)
+    if (base + k < n) local[base + k] = v[k];
+  if (threadIdx.x == 0) tile_total[tile] = total;
+}
+
+// exclusive prefix of the tile totals by one warp: 32-wide Kogge-Stone scans
+// with a running carry (fixed association)
+__device__ __forceinline__ void tile_prefix(const double* __restrict__ tile_total, size_t tiles,
+                                            double* __restrict__ tile_excl) {
+  const int lane = threadIdx.x & 31;
+  double carry = 0.0;
+  for (size_t j0 = 0; j0 < tiles; j0 += 32) {
+    const size_t j = j0 + lane;
+    const double v = j < tiles ? __ldcg(tile_total + j) : 0.0;
+    double inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (j < tiles) tile_excl[j] = carry + (inc - v);
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+// slot m takes the first particle i with cumulative weight >= r + m/n,
+// capped at n-1 (the sequential comb of mcl.cpp:130-140)
+__device__ __forceinline__ void comb_slots(const double* __restrict__ local,
+                                           const double* __restrict__ tile_excl,
+                                           const double* __restrict__ x,
+                                           const double* __restrict__ y,
+                                           const double* __restrict__ t, size_t n,
+                                           size_t out_begin, size_t out_count,
+                                           double* __restrict__ ox, double* __restrict__ oy,
+                                           double* __restrict__ ot, double* __restrict__ ow,
+                                           uint64_t seed, uint64_t iter) {
   double u, unused;
   philox_uniform2(seed, kResampleStream, kResampleStream, iter, u, unused);
   const double r = (1.0 / double(n)) * u;  // uniform_real_distribution(0, 1/n)
@@ -154,7 +208,7 @@ __global__ void k_comb(const double* __restrict__ cdf, const double* __restrict_
     size_t lo = 0, len = n;
     while (len > 0) {
       const size_t half = len >> 1, mid = lo + half;
-      if (cdf[mid] < target) {
+      if (__ldcg(tile_excl + mid / kScanTile) + __ldcg(local + mid) < target) {
         lo = mid + 1;
         len -= half + 1;
       } else {
@@ -169,25 +223,171 @@ __global__ void k_comb(const double* __restrict__ cdf, const double* __restrict_
   }
 }
 
+// ---- stage kernels (sharded step, standalone entry points) ----
+
+// Per-block partial moments; the last block to finish (ticket counter) sums
+// the partials.
+__global__ void __launch_bounds__(kPfThreads) k_weights(
+    const double* __restrict__ logw, const double* __restrict__ gmax,
+    const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ t,
+    size_t n, double* __restrict__ w, double* __restrict__ partial, unsigned* __restrict__ ticket,
+    double* __restrict__ moments) {
+  double acc[10];
+  weight_moments(logw, *gmax, x, y, t, n, w, acc);
+  block_moments(acc, partial);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = threadIdx.x >> 5; k < 10; k += kPfWarps) {
+    const double s = sum_partials(partial, gridDim.x, k);
+    if ((threadIdx.x & 31) == 0) moments[k] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0;
+}
+
+__global__ void k_normalize(double* __restrict__ w, size_t n, const double* __restrict__ moments,
+                            uint64_t n_total, int32_t* __restrict__ degenerate) {
+  const double s = moments[0];
+  const bool bad = degenerate_sum(s);
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    w[i] = bad ? 1.0 / double(n_total) : w[i] / s;
+  if (degenerate && blockIdx.x == 0 && threadIdx.x == 0) *degenerate = bad ? 1 : 0;
+}
+
+// tile scan of already-normalised weights; the last tile to finish writes the
+// tile prefix
+__global__ void __launch_bounds__(kPfThreads) k_tile_scan(
+    const double* __restrict__ w, size_t n, double* __restrict__ local,
+    double* __restrict__ tile_total, double* __restrict__ tile_excl,
+    unsigned* __restrict__ ticket) {
+  __shared__ ScanSmem sm;
+  __shared__ bool last;
+  scan_tile(w, n, blockIdx.x, false, 1.0, false, local, tile_total, sm);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  tile_prefix(tile_total, gridDim.x, tile_excl);
+  if (threadIdx.x == 0) *ticket = 0;
+}
+
+__global__ void k_comb(const double* __restrict__ local, const double* __restrict__ tile_excl,
+                       const double* __restrict__ x, const double* __restrict__ y,
+                       const double* __restrict__ t, size_t n, size_t out_begin,
+                       size_t out_count, double* __restrict__ ox, double* __restrict__ oy,
+                       double* __restrict__ ot, double* __restrict__ ow, uint64_t seed,
+                       uint64_t iter) {
+  comb_slots(local, tile_excl, x, y, t, n, out_begin, out_count, ox, oy, ot, ow, seed, iter);
+}
+
+// ---- the fused step after the sensor model: one cooperative kernel ----
+struct FinishArgs {
+  const double* logw;
+  unsigned long long* gmax_key;
+  double *x, *y, *t, *w;
+  size_t n;
+  double *partial, *local, *tile_total, *tile_excl, *nxyzw;
+  Moments* out;
+  uint64_t seed, iter;
+};
+
+__global__ void __launch_bounds__(kPfThreads, 2) k_pf_finish(FinishArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const size_t n = a.n;
+  // 1. weights and per-block moments
+  {
+    double acc[10];
+    weight_moments(a.logw, order_key_value(*a.gmax_key), a.x, a.y, a.t, n, a.w, acc);
+    block_moments(acc, a.partial);
+  }
+  grid.sync();
+  // 2. every block sums the partials the same way; block 0 publishes them
+  __shared__ double mom[10];
+  for (int k = threadIdx.x >> 5; k < 10; k += kPfWarps) {
+    const double s = sum_partials(a.partial, gridDim.x, k);
+    if ((threadIdx.x & 31) == 0) mom[k] = s;
+  }
+  __syncthreads();
+  const double S = mom[0];
+  const bool bad = degenerate_sum(S);
+  if (blockIdx.x == 0 && threadIdx.x < 10) a.out->m[threadIdx.x] = mom[threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.out->degenerate = bad ? 1 : 0;
+  // 3. normalised tile scans
+  __shared__ ScanSmem sm;
+  const size_t tiles = (n + kScanTile - 1) / kScanTile;
+  for (size_t j = blockIdx.x; j < tiles; j += gridDim.x) {
+    scan_tile(a.w, n, j, true, S, bad, a.local, a.tile_total, sm);
+    __syncthreads();
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32) tile_prefix(a.tile_total, tiles, a.tile_excl);
+  grid.sync();
+  // 4. comb into the scratch set, then copy back over the caller's arrays
+  comb_slots(a.local, a.tile_excl, a.x, a.y, a.t, n, 0, n, a.nxyzw, a.nxyzw + n,
+             a.nxyzw + 2 * n, a.nxyzw + 3 * n, a.seed, a.iter);
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.gmax_key = 0;  // ready for the next step
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    a.x[i] = __ldcg(a.nxyzw + i);
+    a.y[i] = __ldcg(a.nxyzw + n + i);
+    a.t[i] = __ldcg(a.nxyzw + 2 * n + i);
+    a.w[i] = __ldcg(a.nxyzw + 3 * n + i);
+  }
+}
+
+__global__ void k_key_to_double(const unsigned long long* __restrict__ key,
+                                double* __restrict__ out) {
+  *out = order_key_value(*key);
+}
+
+__global__ void k_copy_back(const double* __restrict__ src, double* __restrict__ x,
+                            double* __restrict__ y, double* __restrict__ t,
+                            double* __restrict__ w, size_t n, unsigned long long* reset_key) {
+  if (reset_key && blockIdx.x == 0 && threadIdx.x == 0) *reset_key = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    x[i] = src[i];
+    y[i] = src[n + i];
+    t[i] = src[2 * n + i];
+    w[i] = src[3 * n + i];
+  }
+}
+
 static int blocks(size_t n, int threads = 256, int per_sm = 8) {
   size_t b = (n + threads - 1) / threads;
   return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * per_sm)));
+}
+
+// block count of the moment reduction: a function of n and the SM count only,
+// shared by every path so the sums agree bit for bit
+static int moment_blocks(size_t n) { return blocks(n, kPfThreads, 2); }
+
+static size_t scan_tiles(size_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+static MotionArgs motion_args(double dx, double dy, double dth, const rl_motion_noise_t* noise,
+                              uint64_t seed, uint64_t iter, uint64_t offset) {
+  const double trans = std::hypot(dx, dy);  // mcl.cpp:44-48
+  const double st = std::max(
+      noise->trans_per_trans * trans + noise->trans_per_rot * std::fabs(dth), 1e-12);
+  const double sr = std::max(
+      noise->rot_per_rot * std::fabs(dth) + noise->rot_per_trans * trans, 1e-12);
+  return MotionArgs{dx, dy, dth, st, sr, seed, iter, offset};
 }
 
 // grows c->ws to at least `need` bytes
 static int workspace(rl_cddt* c, size_t need, uint8_t** p) {
   if (c->ws.n < need) RL_TRY(c->ws.alloc(need));
   *p = c->ws.p;
-  return RL_OK;
-}
-
-int weights_launch(const double* logw, const double* gmax, const double* x, const double* y,
-                   const double* t, size_t n, double* w, double* moments, double* partial,
-                   cudaStream_t st) {
-  const int nb = blocks(n, kMomentBlock, 2);
-  k_weights<<<nb, kMomentBlock, 0, st>>>(logw, gmax, x, y, t, n, w, partial);
-  k_sum_partials<<<1, 320, 0, st>>>(partial, nb, moments);
-  RL_CK(cudaGetLastError());
   return RL_OK;
 }
 
@@ -206,14 +406,9 @@ int rl_motion_update(double* x, double* y, double* theta, size_t n, uint64_t ind
     return RL_EINVAL;
   }
   if (n == 0) return RL_OK;
-  const double trans = std::hypot(dx, dy);  // mcl.cpp:44-48
-  const double st = std::max(noise->trans_per_trans * trans + noise->trans_per_rot * std::fabs(dtheta),
-                             1e-12);
-  const double sr = std::max(noise->rot_per_rot * std::fabs(dtheta) + noise->rot_per_trans * trans,
-                             1e-12);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  k_motion<<<blocks(n), 256, 0, s>>>(x, y, theta, n, index_offset, dx, dy, dtheta, st, sr, seed,
-                                    iteration);
+  k_motion<<<blocks(n), 256, 0, s>>>(
+      x, y, theta, n, motion_args(dx, dy, dtheta, noise, seed, iteration, index_offset));
   RL_CK(cudaGetLastError());
   if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
@@ -235,14 +430,19 @@ int rl_pf_weights(const double* logw, const double* gmax, const double* x, const
                   const double* theta, size_t n, double* w, double* moments, void* stream) {
   if (!logw || !gmax || !x || !y || !theta || !w || !moments) return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  DevBuf<double> partial;
-  RL_TRY(partial.alloc(size_t(blocks(n, kMomentBlock, 2)) * 10));
   if (n == 0) {
     RL_CK(cudaMemsetAsync(moments, 0, 10 * sizeof(double), s));
-  } else {
-    RL_TRY(weights_launch(logw, gmax, x, y, theta, n, w, moments, partial.p, s));
+    RL_CK(cudaStreamSynchronize(s));
+    return RL_OK;
   }
-  RL_CK(cudaStreamSynchronize(s));
+  const int nb = moment_blocks(n);
+  DevBuf<double> partial;
+  RL_TRY(partial.alloc(size_t(nb) * 10 + 1));
+  unsigned* ticket = reinterpret_cast<unsigned*>(partial.p + size_t(nb) * 10);
+  RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+  k_weights<<<nb, kPfThreads, 0, s>>>(logw, gmax, x, y, theta, n, w, partial.p, ticket, moments);
+  RL_CK(cudaGetLastError());
+  RL_CK(cudaStreamSynchronize(s));  // partial is freed on return
   return RL_OK;
 }
 
@@ -264,17 +464,17 @@ int rl_resample_low_variance(const double* x, const double* y, const double* the
   if (!x || !y || !theta || !w || !ox || !oy || !otheta || !ow || out_begin + out_count > n)
     return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  size_t bytes = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, bytes, w, (double*)nullptr, int(n), s);
-  DevBuf<uint8_t> tmp;
-  DevBuf<double> cdf;
-  RL_TRY(tmp.alloc(bytes));
-  RL_TRY(cdf.alloc(n));
-  RL_CK(cub::DeviceScan::InclusiveSum(tmp.p, bytes, w, cdf.p, int(n), s));
-  k_comb<<<blocks(out_count), 256, 0, s>>>(cdf.p, x, y, theta, n, out_begin, out_count, ox, oy,
-                                          otheta, ow, seed, iteration);
+  const size_t T = scan_tiles(n);
+  DevBuf<double> tmp;  // local[n] | tile_total[T] | tile_excl[T] | ticket
+  RL_TRY(tmp.alloc(n + 2 * T + 1));
+  double *local = tmp.p, *tile_total = local + n, *tile_excl = tile_total + T;
+  unsigned* ticket = reinterpret_cast<unsigned*>(tile_excl + T);
+  RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+  k_tile_scan<<<int(T), kPfThreads, 0, s>>>(w, n, local, tile_total, tile_excl, ticket);
+  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, x, y, theta, n, out_begin, out_count,
+                                          ox, oy, otheta, ow, seed, iteration);
   RL_CK(cudaGetLastError());
-  RL_CK(cudaStreamSynchronize(s));
+  RL_CK(cudaStreamSynchronize(s));  // tmp is freed on return
   return RL_OK;
 }
 
@@ -284,50 +484,109 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
                 const rl_beam_params_t* params, const float* table, int32_t zdim, double inv_res,
                 uint64_t seed, uint64_t iteration, double* estimate, void* stream) {
   if (!c || !noise || !scan || nbeams <= 0 || (n && (!x || !y || !theta || !w))) return RL_EINVAL;
+  if (n > (1ull << 32)) {
+    set_error("motion_update: particle index exceeds the 32-bit RNG counter");
+    return RL_EINVAL;
+  }
   if (n == 0) return RL_OK;
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
-  // workspace: logw | w2 x y t (resample targets) | cdf | partials | moments | max | flag | cub
-  size_t cub_bytes = 0, b2 = 0;
-  cub::DeviceReduce::Max(nullptr, cub_bytes, (double*)nullptr, (double*)nullptr, int(n), st);
-  cub::DeviceScan::InclusiveSum(nullptr, b2, (double*)nullptr, (double*)nullptr, int(n), st);
-  cub_bytes = std::max(cub_bytes, b2);
-  const int nbw = blocks(n, kMomentBlock, 2);
-  const size_t need = 8 * n * 6 + 8 * size_t(nbw) * 10 + 8 * 16 + cub_bytes + 512;
+  // control (pf_ctl): {gmax key, ticket} | Moments; workspace: logw[n] |
+  // resampled x y t w [4n] | local[n] | tile_total[T] | tile_excl[T] | partial[nbw * 10]
+  struct Control {
+    unsigned long long gmax_key;
+    unsigned ticket;
+  };
+  if (!c->pf_ctl.p) RL_TRY(c->pf_ctl.alloc(256));
+  if (!c->pf_host) RL_CK(cudaMallocHost(&c->pf_host, sizeof(Moments)));
+  const int nbw = moment_blocks(n);
+  const size_t T = scan_tiles(n);
+  const size_t need = 8 * (6 * n + 2 * T + 10 * size_t(nbw));
   uint8_t* base = nullptr;
   RL_TRY(workspace(c, need, &base));
-  double* logw = reinterpret_cast<double*>(base);
-  double* nx = logw + n;
-  double* ny = nx + n;
-  double* nt = ny + n;
-  double* nw = nt + n;
-  double* cdf = nw + n;
-  double* partial = cdf + n;
-  double* moments = partial + size_t(nbw) * 10;
-  double* gmax = moments + 10;
-  int32_t* flag = reinterpret_cast<int32_t*>(gmax + 2);
-  void* tmp = reinterpret_cast<uint8_t*>(gmax + 4);
+  Control* ctl = reinterpret_cast<Control*>(c->pf_ctl.p);
+  Moments* mom = reinterpret_cast<Moments*>(c->pf_ctl.p + 128);
+  FinishArgs fa{};
+  fa.logw = reinterpret_cast<double*>(base);
+  fa.gmax_key = &ctl->gmax_key;
+  fa.x = x;
+  fa.y = y;
+  fa.t = theta;
+  fa.w = w;
+  fa.n = n;
+  fa.nxyzw = const_cast<double*>(fa.logw) + n;
+  fa.local = fa.nxyzw + 4 * n;
+  fa.tile_total = fa.local + n;
+  fa.tile_excl = fa.tile_total + T;
+  fa.partial = fa.tile_excl + T;
+  fa.out = mom;
+  fa.seed = seed;
+  fa.iter = iteration;
 
-  RL_TRY(rl_motion_update(x, y, theta, n, 0, odo_dx, odo_dy, odo_dtheta, noise, seed, iteration,
-                          st));
+#ifdef RL_PF_TRACE
+  static cudaEvent_t ev[5];
+  static bool evi = [] { for (auto& e : ev) cudaEventCreate(&e); return true; }();
+  (void)evi;
+  auto host_t0 = std::chrono::steady_clock::now();
+  cudaEventRecord(ev[0], st);
+#endif
+  if (!c->pf_ctl_clean) RL_CK(cudaMemsetAsync(ctl, 0, sizeof(Control), st));
+  c->pf_ctl_clean = false;
+  const MotionArgs mot = motion_args(odo_dx, odo_dy, odo_dtheta, noise, seed, iteration, 0);
   RL_TRY(sensor_logw_launch(c, x, y, theta, n, scan, nbeams, fov, params, table, zdim, inv_res,
-                            logw, st));
-  RL_CK(cub::DeviceReduce::Max(tmp, cub_bytes, logw, gmax, int(n), st));
-  RL_TRY(weights_launch(logw, gmax, x, y, theta, n, w, moments, partial, st));
-  k_normalize<<<blocks(n), 256, 0, st>>>(w, n, moments, n, flag);
-  RL_CK(cub::DeviceScan::InclusiveSum(tmp, cub_bytes, w, cdf, int(n), st));
-  k_comb<<<blocks(n), 256, 0, st>>>(cdf, x, y, theta, n, 0, n, nx, ny, nt, nw, seed, iteration);
+                            const_cast<double*>(fa.logw), &mot, &ctl->gmax_key, st));
+#ifdef RL_PF_TRACE
+  cudaEventRecord(ev[1], st);
+#endif
+  static const int coop_per_sm = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pf_finish, kPfThreads, 0);
+    return per_sm;
+  }();
+  if (coop_per_sm >= 2) {
+    void* args[] = {&fa};
+    RL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pf_finish), dim3(nbw),
+                                      dim3(kPfThreads), args, 0, st));
+  } else {
+    // same arithmetic as k_pf_finish, stage by stage
+    double* gmax = reinterpret_cast<double*>(c->pf_ctl.p + 64);
+    k_key_to_double<<<1, 1, 0, st>>>(&ctl->gmax_key, gmax);
+    k_weights<<<nbw, kPfThreads, 0, st>>>(fa.logw, gmax, x, y, theta, n, w, fa.partial,
+                                          &ctl->ticket, mom->m);
+    k_normalize<<<blocks(n), 256, 0, st>>>(w, n, mom->m, n, &mom->degenerate);
+    k_tile_scan<<<int(T), kPfThreads, 0, st>>>(w, n, fa.local, fa.tile_total, fa.tile_excl,
+                                               &ctl->ticket);
+    k_comb<<<blocks(n), 256, 0, st>>>(fa.local, fa.tile_excl, x, y, theta, n, 0, n, fa.nxyzw,
+                                      fa.nxyzw + n, fa.nxyzw + 2 * n, fa.nxyzw + 3 * n, seed,
+                                      iteration);
+    k_copy_back<<<blocks(n), 256, 0, st>>>(fa.nxyzw, x, y, theta, w, n, &ctl->gmax_key);
+  }
   RL_CK(cudaGetLastError());
-  RL_CK(cudaMemcpyAsync(x, nx, 8 * n, cudaMemcpyDeviceToDevice, st));
-  RL_CK(cudaMemcpyAsync(y, ny, 8 * n, cudaMemcpyDeviceToDevice, st));
-  RL_CK(cudaMemcpyAsync(theta, nt, 8 * n, cudaMemcpyDeviceToDevice, st));
-  RL_CK(cudaMemcpyAsync(w, nw, 8 * n, cudaMemcpyDeviceToDevice, st));
-  double mom[10];
-  int32_t deg = 0;
-  RL_CK(cudaMemcpyAsync(mom, moments, sizeof mom, cudaMemcpyDeviceToHost, st));
-  RL_CK(cudaMemcpyAsync(&deg, flag, sizeof deg, cudaMemcpyDeviceToHost, st));
+#ifdef RL_PF_TRACE
+  cudaEventRecord(ev[2], st);
+  auto host_t1 = std::chrono::steady_clock::now();
+#endif
+  Moments& h = *static_cast<Moments*>(c->pf_host);
+  RL_CK(cudaMemcpyAsync(&h, mom, sizeof h, cudaMemcpyDeviceToHost, st));
+#ifdef RL_PF_TRACE
+  cudaEventRecord(ev[3], st);
+#endif
   RL_CK(cudaStreamSynchronize(st));
+  c->pf_ctl_clean = true;
+#ifdef RL_PF_TRACE
+  auto host_t2 = std::chrono::steady_clock::now();
+  float a = 0, b = 0, c3 = 0;
+  cudaEventElapsedTime(&a, ev[0], ev[1]);
+  cudaEventElapsedTime(&b, ev[1], ev[2]);
+  cudaEventElapsedTime(&c3, ev[2], ev[3]);
+  fprintf(stderr, "trace memset+sensor %.1f finish %.1f d2h %.1f | host enqueue %.1f total %.1f us\n",
+          a * 1e3, b * 1e3, c3 * 1e3,
+          std::chrono::duration<double, std::micro>(host_t1 - host_t0).count(),
+          std::chrono::duration<double, std::micro>(host_t2 - host_t0).count());
+#endif
+  const double* m = h.m;
+  const bool deg = h.degenerate != 0;
   if (estimate) {
     // Mcl::estimate (mcl.cpp:176-187) on the normalised weights: with
     // normalised w_i = e_i / S the sums are the e-moments divided by S; a
@@ -335,16 +594,16 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
     double sx, sy, sc, ss, sw;
     if (deg) {
       const double inv = 1.0 / double(n);
-      sx = mom[6] * inv;
-      sy = mom[7] * inv;
-      sc = mom[8] * inv;
-      ss = mom[9] * inv;
-      sw = mom[5] * inv;
+      sx = m[6] * inv;
+      sy = m[7] * inv;
+      sc = m[8] * inv;
+      ss = m[9] * inv;
+      sw = m[5] * inv;
     } else {
-      sx = mom[1] / mom[0];
-      sy = mom[2] / mom[0];
-      sc = mom[3] / mom[0];
-      ss = mom[4] / mom[0];
+      sx = m[1] / m[0];
+      sy = m[2] / m[0];
+      sc = m[3] / m[0];
+      ss = m[4] / m[0];
       sw = 1.0;
     }
     if (!(sw > 0.0)) sw = 1.0;

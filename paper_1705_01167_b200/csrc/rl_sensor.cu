@@ -10,11 +10,15 @@
 
 #include <cmath>
 
+#include "pf_device.cuh"
 #include "rl_common.cuh"
 
 namespace rl {
 
-constexpr int kSensorParticlesPerCta = 16;
+#ifndef RL_SENSOR_PB
+#define RL_SENSOR_PB 16
+#endif
+constexpr int kSensorParticlesPerCta = RL_SENSOR_PB;  // particles per CTA (<= 32)
 
 struct BeamParams {
   double w_hit, w_short, w_max, w_rand, sigma_hit, lambda_short, z_max;
@@ -53,40 +57,74 @@ __device__ __forceinline__ int table_index(double r, double inv_res, int zdim) {
   return int(i);
 }
 
+// MOTION: the CTA's particles first take their motion_update step (the fused
+// Mcl::step, mcl.cpp:189-193) and write the moved poses back. gmax_key (may be
+// null) receives the order-preserving atomic max of the log-weights.
+template <bool MOTION>
 __global__ void __launch_bounds__(256) k_sensor_logw(
-    CddtView c, const double* __restrict__ px, const double* __restrict__ py,
-    const double* __restrict__ pt, size_t n, const double* __restrict__ scan, int nb, double fov,
-    BeamParams bp, const float* __restrict__ table, int zdim, double inv_res,
-    double* __restrict__ logw) {
-  extern __shared__ double ll[];  // [PB][nb]
+    CddtView c, double* __restrict__ px, double* __restrict__ py, double* __restrict__ pt,
+    size_t n, const double* __restrict__ scan, int nb, double fov, BeamParams bp,
+    const float* __restrict__ table, int zdim, double inv_res, double* __restrict__ logw,
+    MotionArgs mot, unsigned long long* __restrict__ gmax_key) {
+  extern __shared__ double ll[];  // [PB][nb] log-likelihoods | [nb] beam offsets | [nb] table rows
+  double* boff = ll + kSensorParticlesPerCta * nb;
+  int* mrow = reinterpret_cast<int*>(boff + nb);
+  __shared__ double pose[3][kSensorParticlesPerCta];
   const size_t p0 = size_t(blockIdx.x) * kSensorParticlesPerCta;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    // ScanSpec::beam_offset (mcl.hpp:42-51)
+    boff[b] = nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);
+    if (table) mrow[b] = table_index(scan[b], inv_res, zdim) * zdim;
+  }
+  if (threadIdx.x < kSensorParticlesPerCta) {
+    const size_t i = p0 + threadIdx.x;
+    if (i < n) {
+      double x = px[i], y = py[i], t = pt[i];
+      if (MOTION) {
+        motion_one(mot, uint32_t(mot.index_offset + i), x, y, t);
+        px[i] = x;
+        py[i] = y;
+        pt[i] = t;
+      }
+      pose[0][threadIdx.x] = x;
+      pose[1][threadIdx.x] = y;
+      pose[2][threadIdx.x] = t;
+    }
+  }
+  __syncthreads();
   const int items = kSensorParticlesPerCta * nb;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int pl = it / nb, b = it % nb;
-    const size_t i = p0 + pl;
-    if (i >= n) continue;
-    // ScanSpec::beam_offset (mcl.hpp:42-51)
-    const double off = nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);
-    const double th = normalize_angle_2pi(pt[i] + off);
+    if (p0 + pl >= n) continue;
+    const double th = normalize_angle_2pi(pose[2][pl] + boff[b]);
     CastOut o;
-    const double e = directional_cast(c, px[i], py[i], direction_index(th, c.K), o);
-    const double m = scan[b];
+    const double e = directional_cast(c, pose[0][pl], pose[1][pl], direction_index(th, c.K), o);
     double like;
     if (table)
-      like = double(__ldg(table + size_t(table_index(m, inv_res, zdim)) * zdim +
-                          table_index(e, inv_res, zdim)));
+      like = double(__ldg(table + size_t(unsigned(mrow[b])) + table_index(e, inv_res, zdim)));
     else
-      like = beam_likelihood(bp, e, m);
+      like = beam_likelihood(bp, e, scan[b]);
     ll[it] = log(like);
   }
   __syncthreads();
   if (threadIdx.x < kSensorParticlesPerCta) {
     const size_t i = p0 + threadIdx.x;
+    unsigned long long key = 0;
     if (i < n) {
       double lw = 0.0;
       const double* row = ll + threadIdx.x * nb;
       for (int b = 0; b < nb; b++) lw += row[b];  // mcl.cpp:102-103 order
       logw[i] = lw;
+      key = order_key(lw);
+    }
+    if (gmax_key) {
+#pragma unroll
+      for (int o = kSensorParticlesPerCta / 2; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_down_sync(
+            unsigned((1ull << kSensorParticlesPerCta) - 1), key, o, kSensorParticlesPerCta);
+        key = k2 > key ? k2 : key;
+      }
+      if (threadIdx.x == 0 && key) atomicMax(gmax_key, key);
     }
   }
 }
@@ -115,21 +153,30 @@ static int blocks_for(size_t work, int threads) {
   return int(std::max<size_t>(1, std::min(b, cap)));
 }
 
-int sensor_logw_launch(rl_cddt* c, const double* px, const double* py, const double* pt,
-                       size_t n, const double* scan, int nb, double fov,
-                       const rl_beam_params_t* params, const float* table, int zdim,
-                       double inv_res, double* logw, cudaStream_t st) {
+int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
+                       const double* scan, int nb, double fov, const rl_beam_params_t* params,
+                       const float* table, int zdim, double inv_res, double* logw,
+                       const MotionArgs* mot, unsigned long long* gmax_key, cudaStream_t st) {
   BeamParams bp{};
   if (params)
     bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
                     params->sigma_hit, params->lambda_short, params->z_max};
   const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
-  const size_t smem = sizeof(double) * kSensorParticlesPerCta * nb;
-  if (smem > 48 * 1024)
-    RL_CK(cudaFuncSetAttribute(k_sensor_logw, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
-  k_sensor_logw<<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp, table,
-                                         zdim, inv_res, logw);
+  const size_t smem = sizeof(double) * (kSensorParticlesPerCta + 1) * nb + sizeof(int) * nb;
+  const MotionArgs m = mot ? *mot : MotionArgs{};
+  if (mot) {
+    if (smem > 48 * 1024)
+      RL_CK(cudaFuncSetAttribute(k_sensor_logw<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_sensor_logw<true><<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp,
+                                                 table, zdim, inv_res, logw, m, gmax_key);
+  } else {
+    if (smem > 48 * 1024)
+      RL_CK(cudaFuncSetAttribute(k_sensor_logw<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_sensor_logw<false><<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp,
+                                                  table, zdim, inv_res, logw, m, gmax_key);
+  }
   RL_CK(cudaGetLastError());
   return RL_OK;
 }
@@ -146,8 +193,8 @@ static int check_sensor_args(const rl_cddt* c, const double* px, const double* p
     set_error("beam model z_max must be positive");  // mcl.cpp:13
     return RL_EINVAL;
   }
-  if (table && (zdim <= 0 || !(inv_res > 0.0))) {
-    set_error("likelihood table needs zdim > 0 and inv_res > 0");
+  if (table && (zdim <= 0 || zdim > 32768 || !(inv_res > 0.0))) {
+    set_error("likelihood table needs 0 < zdim <= 32768 and inv_res > 0");
     return RL_EINVAL;
   }
   return RL_OK;
@@ -166,8 +213,9 @@ int rl_sensor_logw(rl_cddt* c, const double* px, const double* py, const double*
   if (!logw && n) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
-  RL_TRY(sensor_logw_launch(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
-                            logw, pick_stream(c, stream)));
+  RL_TRY(sensor_logw_launch(c, const_cast<double*>(px), const_cast<double*>(py),
+                            const_cast<double*>(pt), n, scan, nbeams, fov, params, table, zdim,
+                            inv_res, logw, nullptr, nullptr, pick_stream(c, stream)));
   return finish(c, stream);
 }
 
@@ -234,8 +282,9 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   double* d_sum = d_max + 1;
   int* d_flag = reinterpret_cast<int*>(d_max + 2);
   void* d_tmp = base + 16 * n + 64;
-  RL_TRY(sensor_logw_launch(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
-                            d_logw, st));
+  RL_TRY(sensor_logw_launch(c, const_cast<double*>(px), const_cast<double*>(py),
+                            const_cast<double*>(pt), n, scan, nbeams, fov, params, table, zdim,
+                            inv_res, d_logw, nullptr, nullptr, st));
   RL_CK(cub::DeviceReduce::Max(d_tmp, cub_bytes, d_logw, d_max, int(n), st));
   k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(d_logw, d_max, d_w, n);
   RL_CK(cub::DeviceReduce::Sum(d_tmp, cub_bytes, d_w, d_sum, int(n), st));

@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import RL_EDEGENERATE, check, lib, rl_motion_noise_t
+from ._lib import RL_EDEGENERATE, check, lib, rl_motion_noise_t, torch_stream
 from .rangelib import BeamModelParams, CddtMethod, ScanSpec, kTwoPi, normalize_angle_2pi
 
 
@@ -152,8 +152,7 @@ class Mcl:
             self._scan_dev.copy_(scan, non_blocking=True)
         else:
             self._scan_dev.copy_(torch.from_numpy(np.ascontiguousarray(scan, np.float64)))
-        stream = (C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
-                  if self.dev.type == "cuda" else None)
+        stream = torch_stream(self.dev) if self.dev.type == "cuda" else None
         it = self.iteration
         self.iteration += 1
         if self.world == 1 and self.stages is None:

@@ -21,7 +21,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import LogicError, ParseError, check, lib, rl_beam_params_t, rl_cddt_info_t
+from ._lib import (LogicError, ParseError, check, lib, rl_beam_params_t, rl_cddt_info_t,
+                   torch_stream)
 
 kTwoPi = 6.283185307179586476925286766559  # raycast.hpp:12
 
@@ -139,8 +140,7 @@ def _ptr(a) -> int | None:
 
 
 def _cur_stream(t):
-    import torch
-    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return torch_stream(t.device)
 
 
 @dataclass

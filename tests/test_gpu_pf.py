@@ -159,3 +159,47 @@ def test_mcl_closed_loop_converges(rl, synth):
         r = f.step(*odo[k], scan)
         errs.append(np.hypot(r.estimate.x - pose[k + 1][0], r.estimate.y - pose[k + 1][1]))
     assert np.median(errs[10:]) < 3.0
+
+
+@pytest.mark.parametrize("n", [40_000, 1000, 3, 70_001])
+def test_fused_step_equals_stage_pipeline(rl, synth, n):
+    """rl_mcl_step (motion fused into the sensor kernel, one cooperative
+    finish kernel) equals the stage entry points of the sharded step run on a
+    single rank, bit for bit: the same moment blocks, tile scan and comb."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1705_01167_b200 import _lib, mcl
+    g, pose, px, py, pt, scan = _cfg2(rl, synth, n)
+    method = rl.make_method("cddt", rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(500.0, 120))
+    beam = rl.BeamModelParams(sigma_hit=8.0, z_max=500.0)
+    table = dev(rl.beam_table(beam, 501, 1.0))
+    cfg = mcl.MclConfig(particle_count=n, beam=beam, seed=17,
+                        motion=mcl.MotionNoise(1.0, 0.0, 0.0, 0.02))
+    fused = mcl.Mcl(method, cfg, table=table)
+    staged = mcl.Mcl(method, cfg, table=table)
+    staged.stages = mcl.CudaStages(staged, _lib.torch_stream(staged.dev))
+    for f in (fused, staged):
+        f.set_particles(px, py, pt)
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for k in range(4):
+            a = fused.step(1.0, 0.0, 0.01, scan)
+            b = staged.step(1.0, 0.0, 0.01, scan)
+            assert a.degenerate == b.degenerate
+            assert abs(a.estimate.x - b.estimate.x) <= 1e-9 * max(1.0, abs(b.estimate.x))
+            assert abs(a.estimate.y - b.estimate.y) <= 1e-9 * max(1.0, abs(b.estimate.y))
+            pa, pb = fused.particles(), staged.particles()
+            for key in ("x", "y", "theta", "weight"):
+                np.testing.assert_array_equal(pa[key], pb[key])
+    finally:
+        dist.destroy_process_group()
