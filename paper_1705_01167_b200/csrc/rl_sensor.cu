@@ -57,6 +57,23 @@ __device__ __forceinline__ int table_index(double r, double inv_res, int zdim) {
   return int(i);
 }
 
+// Per-item pieces of the sensor model.
+__device__ __forceinline__ double beam_offset(int b, int nb, double fov) {
+  return nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);  // mcl.hpp:42-51
+}
+
+__device__ __forceinline__ double item_loglike(double e, int b, const double* __restrict__ scan,
+                                               const BeamParams& bp,
+                                               const float* __restrict__ table, int mrow,
+                                               int zdim, double inv_res) {
+  double like;
+  if (table)
+    like = double(__ldg(table + size_t(unsigned(mrow)) + table_index(e, inv_res, zdim)));
+  else
+    like = beam_likelihood(bp, e, scan[b]);
+  return log(like);
+}
+
 // MOTION: the CTA's particles first take their motion_update step (the fused
 // Mcl::step, mcl.cpp:189-193) and write the moved poses back. gmax_key (may be
 // null) receives the order-preserving atomic max of the log-weights.
@@ -73,7 +90,7 @@ __global__ void __launch_bounds__(256) k_sensor_logw(
   const size_t p0 = size_t(blockIdx.x) * kSensorParticlesPerCta;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     // ScanSpec::beam_offset (mcl.hpp:42-51)
-    boff[b] = nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);
+    boff[b] = beam_offset(b, nb, fov);
     if (table) mrow[b] = table_index(scan[b], inv_res, zdim) * zdim;
   }
   if (threadIdx.x < kSensorParticlesPerCta) {
@@ -99,12 +116,7 @@ __global__ void __launch_bounds__(256) k_sensor_logw(
     const double th = normalize_angle_2pi(pose[2][pl] + boff[b]);
     CastOut o;
     const double e = directional_cast(c, pose[0][pl], pose[1][pl], direction_index(th, c.K), o);
-    double like;
-    if (table)
-      like = double(__ldg(table + size_t(unsigned(mrow[b])) + table_index(e, inv_res, zdim)));
-    else
-      like = beam_likelihood(bp, e, scan[b]);
-    ll[it] = log(like);
+    ll[it] = item_loglike(e, b, scan, bp, table, mrow[b], zdim, inv_res);
   }
   __syncthreads();
   if (threadIdx.x < kSensorParticlesPerCta) {
@@ -162,8 +174,8 @@ int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
     bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
                     params->sigma_hit, params->lambda_short, params->z_max};
   const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
-  const size_t smem = sizeof(double) * (kSensorParticlesPerCta + 1) * nb + sizeof(int) * nb;
   const MotionArgs m = mot ? *mot : MotionArgs{};
+  const size_t smem = sizeof(double) * (kSensorParticlesPerCta + 1) * nb + sizeof(int) * nb;
   if (mot) {
     if (smem > 48 * 1024)
       RL_CK(cudaFuncSetAttribute(k_sensor_logw<true>,
@@ -212,6 +224,7 @@ int rl_sensor_logw(rl_cddt* c, const double* px, const double* py, const double*
   RL_TRY(check_sensor_args(c, px, py, pt, n, scan, nbeams, params, table, zdim, inv_res));
   if (!logw && n) return RL_EINVAL;
   if (n == 0) return RL_OK;
+  std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   RL_TRY(sensor_logw_launch(c, const_cast<double*>(px), const_cast<double*>(py),
                             const_cast<double*>(pt), n, scan, nbeams, fov, params, table, zdim,

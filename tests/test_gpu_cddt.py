@@ -520,3 +520,27 @@ def test_concurrent_batches_on_two_streams(rl, synth):
             gpu.cast_batch(*b, out=ob)
     torch.cuda.synchronize()
     assert torch.equal(oa, ra) and torch.equal(ob, rb)
+
+
+def test_default_stream_ordering(rl, synth):
+    """Work queued on torch's default stream before a cast is visible to it:
+    the wrappers pass torch's legacy default stream explicitly (a NULL stream
+    means the handle's own, unordered stream in the C ABI)."""
+    import torch
+    from paper_1705_01167_b200 import _lib
+    assert torch.cuda.current_stream().cuda_stream == 0
+    assert _lib.torch_stream(torch.device("cuda", 0)).value == _lib.CUDA_STREAM_LEGACY
+    g = synth.maze_map(800, 800, 0.1, 2)
+    gpu = make_gpu(rl, g, 120, 300.0)
+    a = [dev(v) for v in synth.free_queries(g, 1_000_000, seed=3)]
+    b = [dev(v) for v in synth.free_queries(g, 1_000_000, seed=4)]
+    want = gpu.cast_batch(*b)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        q = [t.clone() for t in a]
+        torch.cuda._sleep(50_000_000)  # keep the default stream busy (~25 ms)
+        for dst, src in zip(q, b):
+            dst.copy_(src)  # queued behind the sleep
+        got = gpu.cast_batch(*q)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
