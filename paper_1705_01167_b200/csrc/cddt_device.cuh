@@ -43,6 +43,7 @@ struct CddtView {
   int wpr;                                // words per grid row
   const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
   const float* __restrict__ zp;           // zero points, ascending per row
+  const float* __restrict__ hints;        // rows x kHintFloats: each row's first search probes
   const SliceParam* __restrict__ slices;  // S
   const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
   int w, h, K, S;
@@ -68,6 +69,13 @@ __device__ __forceinline__ double div_rn(double a, double d, double r) {
 
 __device__ __forceinline__ double normalize_angle_2pi(double t) {  // raycast.hpp:20-25
   if (t >= 0.0 && t < kTwoPi) return t;  // fmod(t, 2pi) == t exactly here
+  // fmod is exact: on [2pi, 4pi) it is t - 2pi (Sterbenz, so the subtraction
+  // is exact too); on (-2pi, 0) it is t itself, then the reference adds 2pi.
+  if (t >= kTwoPi && t < 2.0 * kTwoPi) return t - kTwoPi;
+  if (t < 0.0 && t > -kTwoPi) {
+    t += kTwoPi;
+    return t >= kTwoPi ? 0.0 : t;
+  }
   t = fmod(t, kTwoPi);
   if (t < 0) t += kTwoPi;
   if (t >= kTwoPi) t = 0.0;
@@ -233,6 +241,83 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
   return first;
 }
 
+// Row search hints: the zero points partition_point probes first in each
+// row, stored per row so they arrive with the row offsets instead of one or
+// more round trips later. Slot layout (floats): [0] level 1, [1..2] level 2,
+// [3..6] level 3 (RL_HINT3), indexed by the decisions taken so far (1 =
+// the probe passed, the search moved right).
+#ifdef RL_HINT3
+constexpr int kHintLevels = 3, kHintFloats = 8;
+#else
+constexpr int kHintLevels = 2, kHintFloats = 4;
+#endif
+
+// index probed at `level` (0-based) after the decisions `path` (level bits,
+// first decision most significant); false when the search ended earlier
+__host__ __device__ __forceinline__ bool hint_index(uint32_t n, int level, uint32_t path,
+                                                   uint32_t* idx) {
+  uint32_t first = 0, len = n;
+  for (int l = 0;; l++) {
+    if (len == 0) return false;
+    const uint32_t half = len >> 1;
+    if (l == level) {
+      *idx = first + half;
+      return true;
+    }
+    if ((path >> (level - 1 - l)) & 1u) {
+      first += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+}
+
+// partition_point with its first kHintLevels steps taken from the row's
+// hints: the same index sequence and comparisons, so the same result.
+__device__ __forceinline__ uint32_t partition_point_hinted(const float* __restrict__ v,
+                                                           uint32_t n, double xq, bool forward,
+                                                           float4 h,
+                                                           const float* __restrict__ hrow) {
+#ifdef RL_AB_NOHINTS
+  return partition_point(v, n, xq, forward);
+#endif
+  const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
+  uint32_t first = 0, len = n, path = 0;
+#pragma unroll
+  for (int l = 0; l < kHintLevels; l++) {
+    if (len == 0) return first;
+    const uint32_t half = len >> 1;
+    float e;
+    if (l == 0) {
+      e = h.x;
+    } else if (l == 1) {
+      e = path ? h.z : h.y;
+    } else {
+      e = __ldg(hrow + 3 + path);  // same sector as h: an L1 hit
+    }
+    const bool pass = forward ? (e <= xlo) : (e < xhi);
+    if (pass) {
+      first += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+    path = (path << 1) | (pass ? 1u : 0u);
+  }
+  while (len > 0) {
+    const uint32_t half = len >> 1, mid = first + half;
+    const float e = __ldg(v + mid);
+    if (forward ? (e <= xlo) : (e < xhi)) {
+      first = mid + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  return first;
+}
+
 // Outcome of one query beyond the range: the occupied cell that settled it
 // and the resolving zero point (what MarkSink::mark receives, cddt.cpp:249,259).
 struct CastOut {
@@ -247,6 +332,7 @@ struct QueryRow {
   double xq;        // projected x' of the query (cddt.hpp:31)
   uint32_t g;       // global row
   uint32_t lo, hi;  // CSR range of the row
+  float4 hint;      // the row's first search hints (slots 0..3)
 };
 __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, double y, int a) {
   QueryRow q;
@@ -262,6 +348,9 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   // requested together with the origin cell's bits: the two are independent
   q.lo = __ldg(c.row_off + q.g);
   q.hi = __ldg(c.row_off + q.g + 1);
+#ifndef RL_AB_NOHINTS
+  q.hint = __ldg(reinterpret_cast<const float4*>(c.hints + size_t(q.g) * kHintFloats));
+#endif
   return q;
 }
 
@@ -309,7 +398,8 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     if (r == kWalkExit) return c.max_range;
   }
   const float* __restrict__ v = c.zp + q.lo;
-  const uint32_t first = partition_point(v, q.hi - q.lo, q.xq, q.forward);
+  const uint32_t first = partition_point_hinted(v, q.hi - q.lo, q.xq, q.forward, q.hint,
+                                                c.hints + size_t(q.g) * kHintFloats);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
   for (int idx = q.forward ? (int)first : (int)first - 1; idx >= 0 && idx < n; idx += step) {
@@ -371,7 +461,9 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
     def->idx = -1;  // near field needs the walker: phase 2 redoes the whole query
     return false;
   }
-  const uint32_t first = partition_point(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward);
+  const uint32_t first =
+      partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint,
+                             c.hints + size_t(q.g) * kHintFloats);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
   const double4 dir = c.dirs[a];

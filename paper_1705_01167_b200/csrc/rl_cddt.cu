@@ -166,6 +166,34 @@ int refresh_query_bits(rl_cddt* c) {
   return RL_OK;
 }
 
+__global__ void k_row_hints(const uint32_t* __restrict__ row_off, const float* __restrict__ zp,
+                            uint64_t rows, float* __restrict__ hints) {
+  for (uint64_t g = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; g < rows;
+       g += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t lo = row_off[g], n = row_off[g + 1] - lo;
+    float h[kHintFloats];
+    int slot = 0;
+    for (int level = 0; level < kHintLevels; level++)
+      for (uint32_t path = 0; path < (1u << level); path++, slot++) {
+        uint32_t idx;
+        h[slot] = hint_index(n, level, path, &idx) ? zp[lo + idx] : 0.f;
+      }
+    for (; slot < kHintFloats; slot++) h[slot] = 0.f;
+    for (int k = 0; k < kHintFloats; k += 4)
+      reinterpret_cast<float4*>(hints + g * kHintFloats)[k / 4] =
+          make_float4(h[k], h[k + 1], h[k + 2], h[k + 3]);
+  }
+}
+
+int refresh_row_hints(rl_cddt* c) {
+  if (c->hints.n != c->rows * kHintFloats) RL_TRY(c->hints.alloc(c->rows * kHintFloats));
+  if (c->rows)
+    k_row_hints<<<int(std::min<uint64_t>((c->rows + 255) / 256, uint64_t(sm_count()) * 16)), 256,
+                  0, c->stream>>>(c->row_off.p, c->zp.p, c->rows, c->hints.p);
+  RL_CK(cudaGetLastError());
+  return RL_OK;
+}
+
 // Compact member cells into an (unordered) edge list; warp-aggregated atomics.
 __global__ void k_edge_list(const uint8_t* __restrict__ flags, size_t n, int32_t* __restrict__ edges,
                             unsigned int* __restrict__ count) {
@@ -319,6 +347,7 @@ int build_structure(rl_cddt* c) {
                                              int(rows), c->row_off.p, c->row_off.p + 1, st));
   }
   RL_TRY(refresh_query_bits(c));
+  RL_TRY(refresh_row_hints(c));
   // host membership mirror
   c->member_h.assign(wh, 0);
   {
@@ -650,6 +679,8 @@ int prune_structure(rl_cddt* c) {
   c->row_off = std::move(noff);
   c->zero_points = kept;
   c->pruned = true;
+  RL_TRY(refresh_row_hints(c));
+  RL_CK(cudaStreamSynchronize(st));
   return RL_OK;
 }
 
@@ -739,6 +770,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->rowbits.release();
     c->row_off.release();
     c->zp.release();
+    c->hints.release();
     c->d_slices.release();
     c->d_dirs.release();
     c->d_scalar.release();
@@ -774,8 +806,9 @@ int rl_cddt_info(const rl_cddt* c, rl_cddt_info_t* o) {
   o->zero_points = c->zero_points;
   const uint64_t wh = uint64_t(c->w) * c->h;
   o->memory_bytes = 4 * c->zero_points + (wh + 7) / 8 + uint64_t(c->S) * 48;  // cddt.hpp:200-203
-  o->device_bytes = c->flags.bytes() + c->row_off.bytes() + 4 * c->zero_points +
-                    c->d_slices.bytes() + c->d_dirs.bytes();
+  o->device_bytes = c->flags.bytes() + c->rowbits.bytes() + c->row_off.bytes() +
+                    c->hints.bytes() + 4 * c->zero_points + c->d_slices.bytes() +
+                    c->d_dirs.bytes();
   o->init_seconds = c->init_seconds;
   return RL_OK;
 }

@@ -115,6 +115,7 @@ struct rl_cddt {
   rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
   int wpr = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
+  rl::DevBuf<float> hints;          // rows x kHintFloats: search hints (cddt_device.cuh)
   rl::DevBuf<float> zp;             // capacity >= zero_points
   rl::DevBuf<rl::SliceParam> d_slices;
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
@@ -135,6 +136,7 @@ struct rl_cddt {
     v.wpr = wpr;
     v.row_off = row_off.p;
     v.zp = zp.p;
+    v.hints = hints.p;
     v.slices = d_slices.p;
     v.dirs = d_dirs.p;
     v.w = w;
@@ -153,4 +155,5 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
 }
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
+int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
 }  // namespace rl

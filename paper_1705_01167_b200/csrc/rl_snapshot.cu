@@ -242,6 +242,7 @@ int rl_cddt_deserialize(const uint8_t* bytes, size_t n, int32_t device, rl_cddt*
     return fail(RL_ECUDA);
   }
   if ((st = refresh_query_bits(c))) return fail(st);
+  if ((st = refresh_row_hints(c))) return fail(st);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail(RL_ECUDA);
   *out = c;
   return RL_OK;

@@ -300,6 +300,7 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   }
   std::swap(c->zp, c->zp_spare);
   std::swap(c->row_off, c->off_spare);
+  RL_TRY(refresh_row_hints(c));
   c->zero_points = total_miss[0];
   return finish(c, nullptr);
 }
