@@ -64,7 +64,11 @@ def build_cuda(force: bool = False, defines: tuple[str, ...] = (), out: Path | N
     if not force and not _stale(lib, cu + hdrs + [Path(__file__)]):
         return lib
     nvcc = _nvcc()
-    objdir = OBJ if not defines else OBJ / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    if not defines and out is None:
+        objdir = OBJ
+    else:  # variant libraries keep their own objects
+        tag = "_".join(d.replace("=", "") for d in defines) or Path(out).stem
+        objdir = OBJ / ("v_" + tag)
     objdir.mkdir(parents=True, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
 

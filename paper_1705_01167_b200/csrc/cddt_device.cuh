@@ -274,20 +274,31 @@ __host__ __device__ __forceinline__ bool hint_index(uint32_t n, int level, uint3
 }
 
 // partition_point with its first kHintLevels steps taken from the row's
-// hints: the same index sequence and comparisons, so the same result.
-__device__ __forceinline__ uint32_t partition_point_hinted(const float* __restrict__ v,
-                                                           uint32_t n, double xq, bool forward,
-                                                           float4 h,
-                                                           const float* __restrict__ hrow) {
+// hints: the same index sequence and comparisons, so the same result. It also
+// reports the first candidate's zero point when the search probed it (the
+// forward candidate is the leftmost failing probe, the backward one the
+// rightmost passing probe), which saves that load for short rows.
+struct RowSearch {
+  uint32_t first;  // partition point
+  uint32_t kidx;   // index whose value is kval (~0u: none)
+  float kval;
+};
+
+__device__ __forceinline__ RowSearch partition_point_hinted(const float* __restrict__ v,
+                                                            uint32_t n, double xq, bool forward,
+                                                            float4 h,
+                                                            const float* __restrict__ hrow) {
+  RowSearch r{0, ~0u, 0.f};
 #ifdef RL_AB_NOHINTS
-  return partition_point(v, n, xq, forward);
+  r.first = partition_point(v, n, xq, forward);
+  return r;
 #endif
   const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
-  uint32_t first = 0, len = n, path = 0;
+  uint32_t len = n, path = 0;
 #pragma unroll
   for (int l = 0; l < kHintLevels; l++) {
-    if (len == 0) return first;
-    const uint32_t half = len >> 1;
+    if (len == 0) return r;
+    const uint32_t half = len >> 1, mid = r.first + half;
     float e;
     if (l == 0) {
       e = h.x;
@@ -297,8 +308,12 @@ __device__ __forceinline__ uint32_t partition_point_hinted(const float* __restri
       e = __ldg(hrow + 3 + path);  // same sector as h: an L1 hit
     }
     const bool pass = forward ? (e <= xlo) : (e < xhi);
+    if (pass != forward) {
+      r.kidx = mid;
+      r.kval = e;
+    }
     if (pass) {
-      first += half + 1;
+      r.first = mid + 1;
       len -= half + 1;
     } else {
       len = half;
@@ -306,16 +321,21 @@ __device__ __forceinline__ uint32_t partition_point_hinted(const float* __restri
     path = (path << 1) | (pass ? 1u : 0u);
   }
   while (len > 0) {
-    const uint32_t half = len >> 1, mid = first + half;
+    const uint32_t half = len >> 1, mid = r.first + half;
     const float e = __ldg(v + mid);
-    if (forward ? (e <= xlo) : (e < xhi)) {
-      first = mid + 1;
+    const bool pass = forward ? (e <= xlo) : (e < xhi);
+    if (pass != forward) {
+      r.kidx = mid;
+      r.kval = e;
+    }
+    if (pass) {
+      r.first = mid + 1;
       len -= half + 1;
     } else {
       len = half;
     }
   }
-  return first;
+  return r;
 }
 
 // Outcome of one query beyond the range: the occupied cell that settled it
@@ -398,13 +418,14 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     if (r == kWalkExit) return c.max_range;
   }
   const float* __restrict__ v = c.zp + q.lo;
-  const uint32_t first = partition_point_hinted(v, q.hi - q.lo, q.xq, q.forward, q.hint,
-                                                c.hints + size_t(q.g) * kHintFloats);
+  const RowSearch rs = partition_point_hinted(v, q.hi - q.lo, q.xq, q.forward, q.hint,
+                                              c.hints + size_t(q.g) * kHintFloats);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
-  for (int idx = q.forward ? (int)first : (int)first - 1; idx >= 0 && idx < n; idx += step) {
+  for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
+       idx += step) {
     // consider(v, index), cddt.cpp:236-262
-    const double vv = (double)__ldg(v + idx);
+    const double vv = (double)(uint32_t(idx) == rs.kidx ? rs.kval : __ldg(v + idx));
     const double d = q.forward ? vv - q.xq : q.xq - vv;
     if (d >= c.max_range) break;
     int32_t cell;
@@ -461,14 +482,15 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
     def->idx = -1;  // near field needs the walker: phase 2 redoes the whole query
     return false;
   }
-  const uint32_t first =
+  const RowSearch rs =
       partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint,
                              c.hints + size_t(q.g) * kHintFloats);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
   const double4 dir = c.dirs[a];
-  for (int idx = q.forward ? (int)first : (int)first - 1; idx >= 0 && idx < n; idx += step) {
-    const double vv = (double)__ldg(c.zp + q.lo + idx);
+  for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
+       idx += step) {
+    const double vv = (double)(uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx));
     const double d = q.forward ? vv - q.xq : q.xq - vv;
     if (d >= c.max_range) break;
     int32_t cell;
