@@ -152,7 +152,7 @@ struct Walker {
   }
   // walker.emplace(...) (place(0)) followed by seek(tt): place() resets the
   // whole state, so this is one place at max(0, tt)
-  __device__ __forceinline__ void init_at(double x, double y, const double4& dir, double tt) {
+  __device__ __forceinline__ void init_params(double x, double y, const double4& dir) {
     ox = x;
     oy = y;
     dx = dir.x;
@@ -167,7 +167,20 @@ struct Walker {
       zx = !(dx > 0) && !(dx < 0);
       zy = !(dy > 0) && !(dy < 0);
     }
+  }
+  __device__ __forceinline__ void init_at(double x, double y, const double4& dir, double tt) {
+    init_params(x, y, dir);
     place(tt > 0.0 ? tt : 0.0);
+  }
+  // the state a previous scan left (tnx/tny are bnd_x(cx)/bnd_y(cy) always)
+  __device__ __forceinline__ void restore(double x, double y, const double4& dir, int ccx,
+                                          int ccy, double tt) {
+    init_params(x, y, dir);
+    t = tt;
+    cx = ccx;
+    cy = ccy;
+    tnx = bnd_x(cx);
+    tny = bnd_y(cy);
   }
   __device__ __forceinline__ void seek(double tt) {  // ray_walker.hpp:36-38
     if (tt > t) place(tt);
@@ -507,33 +520,84 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
 
 // Phase 2 for a deferred window. The origin was clear, so no walker exists
 // yet: emplace + seek(d - kVerifyHalf) is one place(); then the reference's
-// candidate loop continues.
-__device__ __forceinline__ double directional_cast_resume(const CddtView& c, double x, double y,
-                                                          int a, const WalkDefer& def) {
+// candidate loop continues. A query may need many windows (rays grazing a
+// wall meet one failing candidate per wall cell), so the walk kernels scan
+// at most `cap` windows and hand the rest on: WinState is everything the
+// candidate loop carries between iterations (the walker's cell and entry
+// parameter; its boundary parameters are functions of the cell).
+struct WinState {
+  uint32_t lo, n;  // CSR row of the query
+  int idx;         // next candidate
+  int cx, cy;      // walker cell and entry parameter (continuations)
+  double t;
+};
+
+// FRESH: s.idx is phase 1's candidate (landing probe done, no walker yet);
+// otherwise s continues a previous pass (walker restored, s.idx not probed).
+// true: settled, *result set. false: `cap` windows scanned and candidates
+// remain; s continues at s.idx.
+template <bool FRESH>
+__device__ __forceinline__ bool resume_windows(const CddtView& c, double x, double y, int a,
+                                               WinState& s, int cap, double* result) {
   const bool forward = a < c.S;
   const SliceParam sp = c.slices[forward ? a : a - c.S];
   const double xq = x * sp.cos_t + y * sp.sin_t;
   const double4 dir = c.dirs[a];
-  const float* __restrict__ v = c.zp + def.lo;
-  const int n = (int)def.n, step = forward ? 1 : -1;
+  const float* __restrict__ v = c.zp + s.lo;
+  const int n = (int)s.n, step = forward ? 1 : -1;
   Walker<true> wk;
-  for (int idx = def.idx; idx >= 0 && idx < n; idx += step) {
+  int idx = s.idx, windows = 0;
+  if (FRESH) {
+    const double vv = (double)__ldg(v + idx);
+    const double d = forward ? vv - xq : xq - vv;
+    *result = c.max_range;
+    if (d >= c.max_range) return true;
+    wk.init_at(x, y, dir, d - kVerifyHalf);
+    const double r = wk.scan_to(c, d + kVerifyHalf);
+    if (r == kWalkExit) return true;
+    if (r >= 0.0) {
+      *result = d;
+      return true;
+    }
+    windows = 1;
+    idx += step;
+  } else {
+    wk.restore(x, y, dir, s.cx, s.cy, s.t);
+  }
+  for (; idx >= 0 && idx < n; idx += step) {
+    if (windows == cap) {
+      s.idx = idx;
+      s.cx = wk.cx;
+      s.cy = wk.cy;
+      s.t = wk.t;
+      return false;
+    }
     const double vv = (double)__ldg(v + idx);
     const double d = forward ? vv - xq : xq - vv;
     if (d >= c.max_range) break;
-    if (idx == def.idx) {  // phase 1 already ran this candidate's landing probe
-      wk.init_at(x, y, dir, d - kVerifyHalf);
-    } else {
-      int32_t cell;
-      if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) return d;
-      wk.seek(d - kVerifyHalf);
+    int32_t cell;
+    if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {
+      *result = d;
+      return true;
     }
+    wk.seek(d - kVerifyHalf);
     const double r = wk.scan_to(c, d + kVerifyHalf);
+    windows++;
     if (r == kWalkExit) break;
     if (r < 0.0) continue;
-    return d;
+    *result = d;
+    return true;
   }
-  return c.max_range;
+  *result = c.max_range;
+  return true;
+}
+
+__device__ __forceinline__ double directional_cast_resume(const CddtView& c, double x, double y,
+                                                          int a, const WalkDefer& def) {
+  WinState s{def.lo, def.n, def.idx, 0, 0, 0.0};
+  double r;
+  resume_windows<true>(c, x, y, a, s, 0x7fffffff, &r);
+  return r;
 }
 
 }  // namespace rl

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "rl_common.cuh"
@@ -410,6 +411,12 @@ struct __align__(16) WalkRecord {
 #ifndef RL_P2_CTAS
 #define RL_P2_CTAS 4
 #endif
+#ifndef RL_WIN_CAP1
+#define RL_WIN_CAP1 2  // windows per query in the first window pass
+#endif
+#ifndef RL_WIN_CAP2
+#define RL_WIN_CAP2 4  // ... in the second; the third runs to completion
+#endif
 template <class T>
 __global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
     CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
@@ -471,8 +478,8 @@ __global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
   }
 }
 
-// NEAR: records whose origin needs the near-field walk, redone in full;
-// otherwise the pending verification windows, resumed in place.
+// Near-field records, redone in full (NEAR), or (legacy single pass) the
+// pending verification windows resumed to completion.
 template <class T, bool NEAR>
 __global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_defer_p2(CddtView c,
                                                           const WalkRecord* __restrict__ q,
@@ -497,6 +504,102 @@ __global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_defer_p2(CddtView c,
       res = directional_cast_resume(c, x, y, a, WalkDefer{r.lo, r.n, r.idx});
     }
     __stcs(out + r.i, T(res));
+  }
+}
+
+// Window passes. A query needing many verification windows (a ray grazing a
+// wall meets one failing candidate per wall cell) holds its whole warp in a
+// single resume-to-completion pass; instead, pass k scans at most cap_k
+// windows per query and queues the unfinished ones, with the candidate loop's
+// state, for pass k+1 (the last pass has no cap). Each pass is a full-width
+// walk over a shrinking queue.
+struct __align__(16) ContRecord {
+  float x, y, t;
+  uint32_t i, lo, n;
+  int32_t idx, cx, cy, pad;
+  double wt;
+};
+
+// out-of-line: the rare overflow path must not add to the pass's registers
+__device__ __noinline__ double finish_windows(const CddtView& c, double x, double y, int a,
+                                              WinState s) {
+  double res;
+  resume_windows<false>(c, x, y, a, s, 0x7fffffff, &res);
+  return res;
+}
+
+template <class T, bool CONT, bool LAST>
+__global__ void __launch_bounds__(256, RL_P2_CTAS) k_walk_pass(
+    CddtView c, const void* __restrict__ in, const unsigned* __restrict__ in_count,
+    uint32_t in_cap, int cap, ContRecord* __restrict__ oq, unsigned* __restrict__ out_count,
+    uint32_t out_cap, T* __restrict__ out) {
+  __shared__ unsigned cnt_s[8], base_s;
+  // the producer counts every continuation, stored or (queue full) finished
+  const unsigned m = min(*in_count, in_cap);
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (unsigned b0 = blockIdx.x * blockDim.x; b0 < m; b0 += gridDim.x * blockDim.x) {
+    const unsigned k = b0 + threadIdx.x;
+    bool defer = false;
+    float fx = 0.f, fy = 0.f, ft = 0.f;
+    uint32_t qi = 0;
+    WinState s{};
+    int a = 0;
+    if (k < m) {
+      if (CONT) {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const ContRecord*>(in) + k);
+        const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1), w2 = __ldcs(src + 2);
+        fx = w0.x;
+        fy = w0.y;
+        ft = w0.z;
+        qi = __float_as_uint(w0.w);
+        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z),
+                     __float_as_int(w1.w), __float_as_int(w2.x),
+                     __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z))};
+      } else {
+        const float4* src = reinterpret_cast<const float4*>(static_cast<const WalkRecord*>(in) + k);
+        const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1);
+        fx = w0.x;
+        fy = w0.y;
+        ft = w0.z;
+        qi = __float_as_uint(w0.w);
+        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z), 0, 0, 0.0};
+      }
+      a = direction_index(normalize_angle_2pi(double(ft)), c.K);
+      double res;
+      if (resume_windows<!CONT>(c, double(fx), double(fy), a, s, LAST ? 0x7fffffff : cap, &res))
+        __stcs(out + qi, T(res));
+      else
+        defer = true;
+    }
+    if (LAST) continue;
+    const unsigned bal = __ballot_sync(0xffffffffu, defer);
+    if (lane == 0) cnt_s[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < 8; w++) {
+        const unsigned q = cnt_s[w];
+        cnt_s[w] = tot;
+        tot += q;
+      }
+      base_s = tot ? atomicAdd(out_count, tot) : 0u;
+    }
+    __syncthreads();
+    if (defer) {
+      const unsigned slot = base_s + cnt_s[wid] + __popc(bal & ((1u << lane) - 1));
+      if (slot < out_cap) {  // ContRecord layout, as three 16-byte stores
+        float4* dst = reinterpret_cast<float4*>(oq + slot);
+        __stcs(dst, make_float4(fx, fy, ft, __uint_as_float(qi)));
+        __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
+                                    __int_as_float(s.idx), __int_as_float(s.cx)));
+        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
+                                    __int_as_float(__double2loint(s.t)),
+                                    __int_as_float(__double2hiint(s.t))));
+      } else {  // queue full: finish here
+        __stcs(out + qi, T(finish_windows(c, double(fx), double(fy), a, s)));
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -539,18 +642,46 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
       return true;
     }();
     (void)pool_ready;
+    // workspace: counters | n walk records (windows up from 0, near field down
+    // from n-1) | two continuation queues of cap records each
+    // (RL_CDDT_CONT_CAP overrides the queue capacity: a test hook for the
+    // queue-full path)
+    static const size_t cap_env = [] {
+      const char* e = std::getenv("RL_CDDT_CONT_CAP");
+      return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(0);
+    }();
+    const size_t ccap = cap_env ? cap_env : std::max<size_t>(n / 8, size_t(1) << 16);
     uint8_t* ws = nullptr;
-    RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(WalkRecord) * n + 256, st));
-    unsigned* qn = reinterpret_cast<unsigned*>(ws);
+    RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws),
+                          256 + sizeof(WalkRecord) * n + 2 * sizeof(ContRecord) * ccap, st));
+    unsigned* qn = reinterpret_cast<unsigned*>(ws);  // windows, near, cont A, cont B
     WalkRecord* q = reinterpret_cast<WalkRecord*>(ws + 256);
+    ContRecord* ca = reinterpret_cast<ContRecord*>(q + n);
+    ContRecord* cb = ca + ccap;
     static const int p1 = resident_ctas(k_cast_defer_p1<T>);
-    static const int p2 = resident_ctas(k_cast_defer_p2<T, false>);
-    static const int p3 = resident_ctas(k_cast_defer_p2<T, true>);
-    RL_CK(cudaMemsetAsync(qn, 0, 2 * sizeof(unsigned), st));
+    static const int pw1 = resident_ctas(k_walk_pass<T, false, false>);
+    static const int pw2 = resident_ctas(k_walk_pass<T, true, false>);
+    static const int pw3 = resident_ctas(k_walk_pass<T, true, true>);
+    static const int pn = resident_ctas(k_cast_defer_p2<T, true>);
+    RL_CK(cudaMemsetAsync(qn, 0, 4 * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_cast_defer_p2<T, false><<<sm_count() * p2, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
-    k_cast_defer_p2<T, true><<<sm_count() * p3, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+    k_walk_pass<T, false, false><<<sm_count() * pw1, 256, 0, st>>>(
+        v, q, qn, uint32_t(n), RL_WIN_CAP1, ca, qn + 2, uint32_t(ccap), out);
+    k_walk_pass<T, true, false><<<sm_count() * pw2, 256, 0, st>>>(
+        v, ca, qn + 2, uint32_t(ccap), RL_WIN_CAP2, cb, qn + 3, uint32_t(ccap), out);
+    k_walk_pass<T, true, true><<<sm_count() * pw3, 256, 0, st>>>(
+        v, cb, qn + 3, uint32_t(ccap), 0, nullptr, nullptr, 0, out);
+    k_cast_defer_p2<T, true><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+#ifdef RL_DEBUG_COUNTS
+    {
+      unsigned h[4];
+      cudaMemcpyAsync(h, qn, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "counts n=%zu windows=%u near=%u contA=%u contB=%u cap=%zu\n", n, h[0],
+              h[1], h[2], h[3], ccap);
+    }
+#endif
     RL_CK(cudaFreeAsync(ws, st));
     return RL_OK;
   }

@@ -544,3 +544,37 @@ def test_default_stream_ordering(rl, synth):
         got = gpu.cast_batch(*q)
         torch.cuda.synchronize()
         assert torch.equal(got, want)
+
+
+_QUEUE_CHECK = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1705_01167_b200 as rl
+from paper_1705_01167_b200 import synth
+g = synth.polygon_map()
+c = rl.Cddt(rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(1000.0, 200), prune=True)
+q = [torch.from_numpy(a).cuda() for a in synth.free_queries(g, 8_000_000, seed=78)]
+split = c.cast_batch(*q)
+whole = c.cast_batch_f64(*(t.double() for t in q))
+torch.cuda.synchronize()
+print("EQUAL" if torch.equal(split, whole.float()) else "DIFFER")
+"""
+
+
+@pytest.mark.parametrize("cap", ["", "4096", "1"])
+def test_window_pass_queues(cap):
+    """The window passes hand unfinished queries on through bounded queues;
+    with the queue capacity forced tiny (RL_CDDT_CONT_CAP) nearly every
+    continuation takes the queue-full path, which must give the same answers."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    env = dict(os.environ)
+    if cap:
+        env["RL_CDDT_CONT_CAP"] = cap
+    root = str(Path(__file__).resolve().parent.parent)
+    r = subprocess.run([sys.executable, "-c", _QUEUE_CHECK.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("EQUAL"), r.stdout + r.stderr[-2000:]
