@@ -411,11 +411,14 @@ struct __align__(16) WalkRecord {
 #ifndef RL_P2_CTAS
 #define RL_P2_CTAS 4
 #endif
-#ifndef RL_WIN_CAP1
-#define RL_WIN_CAP1 2  // windows per query in the first window pass
+#ifndef RL_WIN_CAPS
+#define RL_WIN_CAPS 1, 2, 4  // windows per query in each capped window pass; a last pass finishes
 #endif
-#ifndef RL_WIN_CAP2
-#define RL_WIN_CAP2 4  // ... in the second; the third runs to completion
+#ifndef RL_CONT_A_DIV
+#define RL_CONT_A_DIV 4  // continuation queue capacities: n / DIV records
+#endif
+#ifndef RL_CONT_B_DIV
+#define RL_CONT_B_DIV 16
 #endif
 template <class T>
 __global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
@@ -643,43 +646,61 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     }();
     (void)pool_ready;
     // workspace: counters | n walk records (windows up from 0, near field down
-    // from n-1) | two continuation queues of cap records each
+    // from n-1) | continuation queues A and B (the window passes alternate)
     // (RL_CDDT_CONT_CAP overrides the queue capacity: a test hook for the
     // queue-full path)
     static const size_t cap_env = [] {
       const char* e = std::getenv("RL_CDDT_CONT_CAP");
       return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(0);
     }();
-    const size_t ccap = cap_env ? cap_env : std::max<size_t>(n / 8, size_t(1) << 16);
+#ifdef RL_WIN_CAPS_CODE  // A/B builds: decimal digits, e.g. 1124 -> {1, 1, 2, 4}
+    constexpr int kPasses = RL_WIN_CAPS_CODE >= 1000 ? 4 : RL_WIN_CAPS_CODE >= 100 ? 3
+                                                     : RL_WIN_CAPS_CODE >= 10 ? 2 : 1;
+    int kCaps[kPasses];
+    for (int p = kPasses - 1, v = RL_WIN_CAPS_CODE; p >= 0; p--, v /= 10) kCaps[p] = v % 10;
+#else
+    constexpr int kCaps[] = {RL_WIN_CAPS};
+    constexpr int kPasses = sizeof(kCaps) / sizeof(kCaps[0]);  // capped passes; one more runs out
+#endif
+    const size_t cap_a = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_A_DIV, size_t(1) << 16);
+    const size_t cap_b = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_B_DIV, size_t(1) << 16);
     uint8_t* ws = nullptr;
     RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws),
-                          256 + sizeof(WalkRecord) * n + 2 * sizeof(ContRecord) * ccap, st));
-    unsigned* qn = reinterpret_cast<unsigned*>(ws);  // windows, near, cont A, cont B
+                          256 + sizeof(WalkRecord) * n + sizeof(ContRecord) * (cap_a + cap_b),
+                          st));
+    unsigned* qn = reinterpret_cast<unsigned*>(ws);  // windows, near, one per capped pass
     WalkRecord* q = reinterpret_cast<WalkRecord*>(ws + 256);
-    ContRecord* ca = reinterpret_cast<ContRecord*>(q + n);
-    ContRecord* cb = ca + ccap;
+    ContRecord* qa = reinterpret_cast<ContRecord*>(q + n);
+    ContRecord* qb = qa + cap_a;
     static const int p1 = resident_ctas(k_cast_defer_p1<T>);
-    static const int pw1 = resident_ctas(k_walk_pass<T, false, false>);
-    static const int pw2 = resident_ctas(k_walk_pass<T, true, false>);
-    static const int pw3 = resident_ctas(k_walk_pass<T, true, true>);
+    static const int pw0 = resident_ctas(k_walk_pass<T, false, false>);
+    static const int pwc = resident_ctas(k_walk_pass<T, true, false>);
+    static const int pwl = resident_ctas(k_walk_pass<T, true, true>);
     static const int pn = resident_ctas(k_cast_defer_p2<T, true>);
-    RL_CK(cudaMemsetAsync(qn, 0, 4 * sizeof(unsigned), st));
+    RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_walk_pass<T, false, false><<<sm_count() * pw1, 256, 0, st>>>(
-        v, q, qn, uint32_t(n), RL_WIN_CAP1, ca, qn + 2, uint32_t(ccap), out);
-    k_walk_pass<T, true, false><<<sm_count() * pw2, 256, 0, st>>>(
-        v, ca, qn + 2, uint32_t(ccap), RL_WIN_CAP2, cb, qn + 3, uint32_t(ccap), out);
-    k_walk_pass<T, true, true><<<sm_count() * pw3, 256, 0, st>>>(
-        v, cb, qn + 3, uint32_t(ccap), 0, nullptr, nullptr, 0, out);
+    k_walk_pass<T, false, false><<<sm_count() * pw0, 256, 0, st>>>(
+        v, q, qn, uint32_t(n), kCaps[0], qa, qn + 2, uint32_t(cap_a), out);
+    for (int p = 1; p < kPasses; p++) {  // queue p-1 -> queue p (A, B, A, ...)
+      const bool from_a = (p & 1) != 0;
+      k_walk_pass<T, true, false><<<sm_count() * pwc, 256, 0, st>>>(
+          v, from_a ? qa : qb, qn + 1 + p, uint32_t(from_a ? cap_a : cap_b), kCaps[p],
+          from_a ? qb : qa, qn + 2 + p, uint32_t(from_a ? cap_b : cap_a), out);
+    }
+    const bool last_a = (kPasses & 1) != 0;
+    k_walk_pass<T, true, true><<<sm_count() * pwl, 256, 0, st>>>(
+        v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
+        nullptr, 0, out);
     k_cast_defer_p2<T, true><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
 #ifdef RL_DEBUG_COUNTS
     {
-      unsigned h[4];
+      unsigned h[2 + kPasses];
       cudaMemcpyAsync(h, qn, sizeof h, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      fprintf(stderr, "counts n=%zu windows=%u near=%u contA=%u contB=%u cap=%zu\n", n, h[0],
-              h[1], h[2], h[3], ccap);
+      fprintf(stderr, "counts n=%zu windows=%u near=%u", n, h[0], h[1]);
+      for (int p = 0; p < kPasses; p++) fprintf(stderr, " after pass %d: %u", p, h[2 + p]);
+      fprintf(stderr, "\n");
     }
 #endif
     RL_CK(cudaFreeAsync(ws, st));
