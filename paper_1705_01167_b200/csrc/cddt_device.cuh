@@ -43,7 +43,7 @@ struct CddtView {
   int wpr;                                // words per grid row
   const uint32_t* __restrict__ row_off;   // rows+1, CSR into zp
   const float* __restrict__ zp;           // zero points, ascending per row
-  const float* __restrict__ hints;        // rows x kHintFloats: each row's first search probes
+  const float* __restrict__ hints;        // rows x kHintFloats: row records (CSR range + probes)
   const SliceParam* __restrict__ slices;  // S
   const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
   int w, h, K, S;
@@ -254,16 +254,14 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
   return first;
 }
 
-// Row search hints: the zero points partition_point probes first in each
-// row, stored per row so they arrive with the row offsets instead of one or
-// more round trips later. Slot layout (floats): [0] level 1, [1..2] level 2,
-// [3..6] level 3 (RL_HINT3), indexed by the decisions taken so far (1 =
-// the probe passed, the search moved right).
-#ifdef RL_HINT3
+// Row records: one 32-byte sector per row with the CSR range and the zero
+// points the row's binary search probes first, so a query's first three
+// search steps arrive with its row instead of one round trip each:
+//   lo, n (u32 bits), L1, L2(0), L2(1), L3(00), L3(01), L3(10)
+// indexed by the decisions taken so far (1 = the probe passed, the search
+// moved right); L3(11) falls back to a zero-point load. Derived from row_off
+// and zp after every structure change (refresh_row_hints).
 constexpr int kHintLevels = 3, kHintFloats = 8;
-#else
-constexpr int kHintLevels = 2, kHintFloats = 4;
-#endif
 
 // index probed at `level` (0-based) after the decisions `path` (level bits,
 // first decision most significant); false when the search ended earlier
@@ -299,13 +297,8 @@ struct RowSearch {
 
 __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restrict__ v,
                                                             uint32_t n, double xq, bool forward,
-                                                            float4 h,
-                                                            const float* __restrict__ hrow) {
+                                                            float4 h, float4 h2) {
   RowSearch r{0, ~0u, 0.f};
-#ifdef RL_AB_NOHINTS
-  r.first = partition_point(v, n, xq, forward);
-  return r;
-#endif
   const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
   uint32_t len = n, path = 0;
 #pragma unroll
@@ -314,11 +307,11 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
     const uint32_t half = len >> 1, mid = r.first + half;
     float e;
     if (l == 0) {
-      e = h.x;
+      e = h.z;
     } else if (l == 1) {
-      e = path ? h.z : h.y;
+      e = path ? h2.x : h.w;
     } else {
-      e = __ldg(hrow + 3 + path);  // same sector as h: an L1 hit
+      e = path == 0 ? h2.y : path == 1 ? h2.z : path == 2 ? h2.w : __ldg(v + mid);
     }
     const bool pass = forward ? (e <= xlo) : (e < xhi);
     if (pass != forward) {
@@ -365,7 +358,7 @@ struct QueryRow {
   double xq;        // projected x' of the query (cddt.hpp:31)
   uint32_t g;       // global row
   uint32_t lo, hi;  // CSR range of the row
-  float4 hint;      // the row's first search hints (slots 0..3)
+  float4 hint, hint2;  // the row record
 };
 __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, double y, int a) {
   QueryRow q;
@@ -379,11 +372,11 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   q.g = sp.row_base + (uint32_t)row;
   // requested together with the origin cell's bits: the two are independent
-  q.lo = __ldg(c.row_off + q.g);
-  q.hi = __ldg(c.row_off + q.g + 1);
-#ifndef RL_AB_NOHINTS
-  q.hint = __ldg(reinterpret_cast<const float4*>(c.hints + size_t(q.g) * kHintFloats));
-#endif
+  const float4* rec = reinterpret_cast<const float4*>(c.hints + size_t(q.g) * kHintFloats);
+  q.hint = __ldg(rec);
+  q.hint2 = __ldg(rec + 1);
+  q.lo = __float_as_uint(q.hint.x);
+  q.hi = q.lo + __float_as_uint(q.hint.y);
   return q;
 }
 
@@ -431,8 +424,8 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     if (r == kWalkExit) return c.max_range;
   }
   const float* __restrict__ v = c.zp + q.lo;
-  const RowSearch rs = partition_point_hinted(v, q.hi - q.lo, q.xq, q.forward, q.hint,
-                                              c.hints + size_t(q.g) * kHintFloats);
+  const RowSearch rs =
+      partition_point_hinted(v, q.hi - q.lo, q.xq, q.forward, q.hint, q.hint2);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
   for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
@@ -496,8 +489,7 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
     return false;
   }
   const RowSearch rs =
-      partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint,
-                             c.hints + size_t(q.g) * kHintFloats);
+      partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint, q.hint2);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
   const double4 dir = c.dirs[a];

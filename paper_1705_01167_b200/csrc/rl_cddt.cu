@@ -174,8 +174,10 @@ __global__ void k_row_hints(const uint32_t* __restrict__ row_off, const float* _
     const uint32_t lo = row_off[g], n = row_off[g + 1] - lo;
     float h[kHintFloats];
     int slot = 0;
+    h[slot++] = __uint_as_float(lo);
+    h[slot++] = __uint_as_float(n);
     for (int level = 0; level < kHintLevels; level++)
-      for (uint32_t path = 0; path < (1u << level); path++, slot++) {
+      for (uint32_t path = 0; path < (1u << level) && slot < kHintFloats; path++, slot++) {
         uint32_t idx;
         h[slot] = hint_index(n, level, path, &idx) ? zp[lo + idx] : 0.f;
       }
