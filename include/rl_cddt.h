@@ -147,6 +147,19 @@ int rl_exact_cast_batch(rl_cddt *c, const double *x, const double *y, const doub
  * (2 * width * height * theta_disc bytes). */
 int rl_lut_build(rl_cddt *c, int32_t theta_disc, uint16_t *entries, void *stream);
 
+/* simulate_scan (proj/src/mcl.cpp:144-154) for n poses at once on the
+ * handle's grid: scan[i * nbeams + b] = clamp(oracle_cast(x_i, y_i, theta_i +
+ * beam_offset(b), max_range) + noise, 0, max_range), beam_offset as
+ * ScanSpec::beam_offset (mcl.hpp:42-51), noise ~ N(0, max(noise_sigma,
+ * 1e-12)) from the counter generator (seed, stream_id, pose, beam) — the
+ * reference's std::normal_distribution stream is implementation-defined.
+ * cos_t/sin_t (optional, n * nbeams each) give each beam's direction as in
+ * rl_exact_cast_batch. Device pointers. */
+int rl_simulate_scans(rl_cddt *c, const double *x, const double *y, const double *theta,
+                      size_t n, int32_t nbeams, double fov, double max_range,
+                      double noise_sigma, uint64_t seed, uint64_t stream_id,
+                      const double *cos_t, const double *sin_t, double *scan, void *stream);
+
 /* Wait for all work queued on the handle's stream. */
 int rl_cddt_sync(rl_cddt *c);
 

@@ -78,6 +78,8 @@ _SIG = {
                                    _P, _P]),
     "rl_exact_cast_batch": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "rl_lut_build": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "rl_simulate_scans": (C.c_int, [_P, _P, _P, _P, C.c_size_t, C.c_int32, C.c_double, C.c_double,
+                                    C.c_double, C.c_uint64, C.c_uint64, _P, _P, _P, _P]),
     "rl_sensor_logw": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,
                                  C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double, _P, _P]),
     "rl_motion_update": (C.c_int, [_P, _P, _P, C.c_size_t, C.c_uint64, C.c_double, C.c_double,

@@ -9,9 +9,11 @@
 // bit parity the caller passes glibc values (cos_t/sin_t); with NULL the
 // device computes them with sincos() (within 1 ulp of glibc). lut_build's K
 // lattice directions are always host glibc values.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
+#include "pf_device.cuh"
 #include "rl_common.cuh"
 
 namespace rl {
@@ -63,6 +65,36 @@ __global__ void k_lut(CddtView c, const double2* __restrict__ dirs, int K,
   }
 }
 
+// simulate_scan (mcl.cpp:144-154), one thread per (pose, beam)
+__global__ void k_scans(CddtView c, const double* __restrict__ px, const double* __restrict__ py,
+                        const double* __restrict__ pt, uint64_t n, int nb, double fov,
+                        double sigma, uint64_t seed, uint64_t stream_id,
+                        const double* __restrict__ cs, const double* __restrict__ sn,
+                        double* __restrict__ scan) {
+  const uint64_t total = n * uint64_t(nb);
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < total;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = k / uint64_t(nb);
+    const int b = int(k - i * uint64_t(nb));
+    double cv, sv;
+    if (cs) {
+      cv = cs[k];
+      sv = sn[k];
+    } else {
+      // RayQuery(x, y, theta + beam_offset(b)) normalises the angle (raycast.hpp:47)
+      const double off = nb <= 1 ? 0.0 : -fov / 2.0 + fov * double(b) / double(nb - 1);
+      sincos(normalize_angle_2pi(pt[i] + off), &sv, &cv);
+    }
+    const double d = exact_cast(c, px[i], py[i], cv, sv);
+    // N(0, sigma): Box-Muller on one Philox draw keyed by (pose, beam)
+    double u0, u1;
+    philox_uniform2(seed, uint32_t(k), uint32_t(k >> 32), stream_id, u0, u1);
+    const double z = sqrt(-2.0 * log(1.0 - u0)) * cos(kTwoPi * u1);
+    const double v = d + sigma * z;
+    scan[k] = v < 0.0 ? 0.0 : (c.max_range < v ? c.max_range : v);  // std::clamp
+  }
+}
+
 static int blocks(uint64_t n) {
   const uint64_t b = (n + 255) / 256, cap = uint64_t(sm_count()) * 8;
   return int(b < 1 ? 1 : (b > cap ? cap : b));
@@ -83,6 +115,26 @@ int rl_exact_cast_batch(rl_cddt* c, const double* x, const double* y, const doub
   DeviceGuard guard(c->dev);
   k_exact<<<blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, theta, cos_t, sin_t,
                                                          out, n);
+  return finish(c, stream);
+}
+
+int rl_simulate_scans(rl_cddt* c, const double* x, const double* y, const double* theta,
+                      size_t n, int32_t nbeams, double fov, double max_range,
+                      double noise_sigma, uint64_t seed, uint64_t stream_id,
+                      const double* cos_t, const double* sin_t, double* scan, void* stream) {
+  if (!c || nbeams <= 0 || !(max_range >= 0.0) || (!cos_t != !sin_t) ||
+      (n && (!x || !y || !scan || (!theta && !cos_t)))) {
+    set_error("simulate_scan: invalid arguments");
+    return RL_EINVAL;
+  }
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  CddtView v = c->view();
+  v.max_range = max_range;  // oracle_cast's own max_range argument
+  const uint64_t total = uint64_t(n) * uint64_t(nbeams);
+  k_scans<<<blocks(total), 256, 0, pick_stream(c, stream)>>>(
+      v, x, y, theta, n, nbeams, fov, std::max(noise_sigma, 1e-12), seed, stream_id, cos_t,
+      sin_t, scan);
   return finish(c, stream);
 }
 

@@ -351,6 +351,22 @@ class Cddt:
                                         _ptr(sin_t), _ptr(out), x.numel(), s))
         return out
 
+    def simulate_scans(self, x, y, theta, spec: "ScanSpec", max_range: float,
+                       noise_sigma: float = 0.0, seed: int = 0, stream_id: int = 0,
+                       cos_t=None, sin_t=None, out=None, stream=None):
+        """simulate_scan (mcl.cpp:144-154) for a batch of poses on this grid:
+        torch CUDA f64 poses -> [n, beam_count] scans. Noise comes from the
+        counter generator (seed, stream_id, pose, beam)."""
+        import torch
+        n = x.numel()
+        if out is None:
+            out = torch.empty((n, spec.beam_count), dtype=torch.float64, device=x.device)
+        s = stream if stream is not None else _cur_stream(x)
+        check(lib().rl_simulate_scans(self._h, _ptr(x), _ptr(y), _ptr(theta), n, spec.beam_count,
+                                      spec.fov, float(max_range), float(noise_sigma), seed,
+                                      stream_id, _ptr(cos_t), _ptr(sin_t), _ptr(out), s))
+        return out
+
     def lut_build(self, theta_disc: int):
         """lut_build (raycast.cpp:62-87) on the GPU: uint16 [theta_disc, h, w] (torch CUDA)."""
         import torch

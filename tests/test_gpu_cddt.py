@@ -453,6 +453,44 @@ def test_lut_build_vs_reference(rl, oracle_mod, synth):
         assert np.array_equal(host(got).view(np.uint16), ref.lut_build(K))
 
 
+def test_simulate_scans_vs_reference(rl, oracle_mod, synth):
+    """simulate_scan (mcl.cpp:144-154) batched: noise-free beams equal the
+    reference oracle_cast; the counter-generator noise is N(0, sigma),
+    reproducible per (seed, stream_id) and clamped to [0, max_range]."""
+    import math
+    import torch
+    if not oracle_mod.ref_available():
+        pytest.skip("reference not compiled")
+    g = synth.rect_map(120, 90, 8, seed=5)
+    spec = rl.ScanSpec(61, 4.71238898038469)
+    rng = np.random.default_rng(12)
+    n = 500
+    x, y, t = rng.uniform(1, 119, n), rng.uniform(1, 89, n), rng.uniform(-7, 13, n)
+    off = np.array([spec.beam_offset(b) for b in range(spec.beam_count)])
+    tb = (t[:, None] + off[None, :]).ravel()
+    tn = np.array([rl.normalize_angle_2pi(v) for v in tb])
+    cs = np.array([math.cos(v) for v in tn])
+    sn = np.array([math.sin(v) for v in tn])
+    xr, yr = np.repeat(x, spec.beam_count), np.repeat(y, spec.beam_count)
+    for mr in (60.0, 25.0):
+        gpu = make_gpu(rl, g, 36, 60.0)  # oracle_cast takes max_range per call
+        want = oracle_mod.RefCddt(g, 36, mr).oracle_batch(xr, yr, tb).reshape(n, -1)
+        clean = gpu.simulate_scans(dev(x), dev(y), dev(t), spec, mr, 0.0, cos_t=dev(cs),
+                                   sin_t=dev(sn))
+        torch.cuda.synchronize()
+        assert np.abs(host(clean) - want).max() <= 1e-9  # the 1e-12 noise floor
+    noisy = gpu.simulate_scans(dev(x), dev(y), dev(t), spec, 25.0, 2.0, seed=3)
+    again = gpu.simulate_scans(dev(x), dev(y), dev(t), spec, 25.0, 2.0, seed=3)
+    other = gpu.simulate_scans(dev(x), dev(y), dev(t), spec, 25.0, 2.0, seed=3, stream_id=1)
+    torch.cuda.synchronize()
+    nz, cl = host(noisy), want
+    assert np.array_equal(nz, host(again)) and not np.array_equal(nz, host(other))
+    assert nz.min() >= 0.0 and nz.max() <= 25.0
+    inner = (cl > 8.0) & (cl < 17.0)  # far from both clamps
+    r = (nz - cl)[inner]
+    assert r.size > 2000 and abs(r.mean()) < 0.15 and abs(r.std() - 2.0) < 0.1
+
+
 # ---- the deferred-walk batch path (f32, >= 4M queries) ----
 def _deferred_vs_oracle(rl, oracle_mod, g, K, mr, qx, qy, qt):
     import torch
