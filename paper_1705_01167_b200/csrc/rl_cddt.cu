@@ -422,13 +422,17 @@ struct __align__(16) WalkRecord {
 #ifndef RL_CONT_B_DIV
 #define RL_CONT_B_DIV 16
 #endif
+#ifndef RL_P1_THREADS
+#define RL_P1_THREADS 64  // small CTAs: the per-iteration compaction barrier waits for fewer warps
+#endif
+constexpr int kP1Threads = RL_P1_THREADS, kP1Warps = kP1Threads / 32;
 template <class T>
-__global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
+__global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_cast_defer_p1(
     CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
     T* __restrict__ out, uint32_t n, WalkRecord* __restrict__ q, unsigned* __restrict__ qn) {
   // queue layout: window records grow up from q[0], near-field records down
   // from q[n-1]; qn[0], qn[1] count them
-  __shared__ unsigned cnt_s[2][8], base_s[2];
+  __shared__ unsigned cnt_s[2][kP1Warps], base_s[2];
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n; b0 += gridDim.x * blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(256, RL_P1_CTAS) k_cast_defer_p1(
     __syncthreads();
     if (threadIdx.x < 2) {
       unsigned tot = 0;
-      for (int w = 0; w < 8; w++) {
+      for (int w = 0; w < kP1Warps; w++) {
         const unsigned k = cnt_s[threadIdx.x][w];
         cnt_s[threadIdx.x][w] = tot;
         tot += k;
@@ -525,6 +529,11 @@ struct __align__(16) ContRecord {
   double wt;
 };
 
+#ifndef RL_WALK_THREADS
+#define RL_WALK_THREADS 64  // small CTAs: cheap compaction barriers
+#endif
+constexpr int kWalkThreads = RL_WALK_THREADS;
+
 // out-of-line: the rare overflow path must not add to the pass's registers
 __device__ __noinline__ double finish_windows(const CddtView& c, double x, double y, int a,
                                               WinState s) {
@@ -534,11 +543,11 @@ __device__ __noinline__ double finish_windows(const CddtView& c, double x, doubl
 }
 
 template <class T, bool CONT, bool LAST>
-__global__ void __launch_bounds__(256, RL_P2_CTAS) k_walk_pass(
+__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_walk_pass(
     CddtView c, const void* __restrict__ in, const unsigned* __restrict__ in_count,
     uint32_t in_cap, int cap, ContRecord* __restrict__ oq, unsigned* __restrict__ out_count,
     uint32_t out_cap, T* __restrict__ out) {
-  __shared__ unsigned cnt_s[8], base_s;
+  __shared__ unsigned cnt_s[kWalkThreads / 32], base_s;
   // the producer counts every continuation, stored or (queue full) finished
   const unsigned m = min(*in_count, in_cap);
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -582,7 +591,7 @@ __global__ void __launch_bounds__(256, RL_P2_CTAS) k_walk_pass(
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned tot = 0;
-      for (int w = 0; w < 8; w++) {
+      for (int w = 0; w < kWalkThreads / 32; w++) {
         const unsigned q = cnt_s[w];
         cnt_s[w] = tot;
         tot += q;
@@ -674,24 +683,34 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     WalkRecord* q = reinterpret_cast<WalkRecord*>(ws + 256);
     ContRecord* qa = reinterpret_cast<ContRecord*>(q + n);
     ContRecord* qb = qa + cap_a;
-    static const int p1 = resident_ctas(k_cast_defer_p1<T>);
-    static const int pw0 = resident_ctas(k_walk_pass<T, false, false>);
-    static const int pwc = resident_ctas(k_walk_pass<T, true, false>);
-    static const int pwl = resident_ctas(k_walk_pass<T, true, true>);
+    static const int p1 = [] {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast_defer_p1<T>, kP1Threads, 0);
+      return std::max(per_sm, 1);
+    }();
+    auto walk_ctas = [](auto kernel) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWalkThreads, 0);
+      return std::max(per_sm, 1);
+    };
+    static const int pw0 = walk_ctas(k_walk_pass<T, false, false>);
+    static const int pwc = walk_ctas(k_walk_pass<T, true, false>);
+    static const int pwl = walk_ctas(k_walk_pass<T, true, true>);
     static const int pn = resident_ctas(k_cast_defer_p2<T, true>);
     RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
-    const size_t b1 = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * p1));
-    k_cast_defer_p1<T><<<int(b1), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_walk_pass<T, false, false><<<sm_count() * pw0, 256, 0, st>>>(
+    const size_t b1 = std::max<size_t>(
+        1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
+    k_cast_defer_p1<T><<<int(b1), kP1Threads, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
+    k_walk_pass<T, false, false><<<sm_count() * pw0, kWalkThreads, 0, st>>>(
         v, q, qn, uint32_t(n), kCaps[0], qa, qn + 2, uint32_t(cap_a), out);
     for (int p = 1; p < kPasses; p++) {  // queue p-1 -> queue p (A, B, A, ...)
       const bool from_a = (p & 1) != 0;
-      k_walk_pass<T, true, false><<<sm_count() * pwc, 256, 0, st>>>(
+      k_walk_pass<T, true, false><<<sm_count() * pwc, kWalkThreads, 0, st>>>(
           v, from_a ? qa : qb, qn + 1 + p, uint32_t(from_a ? cap_a : cap_b), kCaps[p],
           from_a ? qb : qa, qn + 2 + p, uint32_t(from_a ? cap_b : cap_a), out);
     }
     const bool last_a = (kPasses & 1) != 0;
-    k_walk_pass<T, true, true><<<sm_count() * pwl, 256, 0, st>>>(
+    k_walk_pass<T, true, true><<<sm_count() * pwl, kWalkThreads, 0, st>>>(
         v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
         nullptr, 0, out);
     k_cast_defer_p2<T, true><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
