@@ -262,6 +262,10 @@ __device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v,
 // moved right); L3(11) falls back to a zero-point load. Derived from row_off
 // and zp after every structure change (refresh_row_hints).
 constexpr int kHintLevels = 3, kHintFloats = 8;
+#ifndef RL_LINEAR_TAIL
+#define RL_LINEAR_TAIL 4
+#endif
+constexpr int kLinearTail = RL_LINEAR_TAIL;  // rows searched by one parallel load at the end
 
 // index probed at `level` (0-based) after the decisions `path` (level bits,
 // first decision most significant); false when the search ended earlier
@@ -326,7 +330,7 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
     }
     path = (path << 1) | (pass ? 1u : 0u);
   }
-  while (len > 0) {
+  while (len > kLinearTail) {
     const uint32_t half = len >> 1, mid = r.first + half;
     const float e = __ldg(v + mid);
     const bool pass = forward ? (e <= xlo) : (e < xhi);
@@ -340,6 +344,26 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
     } else {
       len = half;
     }
+  }
+  if (kLinearTail > 0 && len > 0) {
+    // the last <= kLinearTail elements in one round trip: the partition point
+    // is the count of passing elements (the predicate is monotone)
+    float e[kLinearTail > 0 ? kLinearTail : 1];
+#pragma unroll
+    for (int k = 0; k < kLinearTail; k++) e[k] = uint32_t(k) < len ? __ldg(v + r.first + k) : 0.f;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kLinearTail; k++)
+      cnt += (uint32_t(k) < len && (forward ? (e[k] <= xlo) : (e[k] < xhi))) ? 1u : 0u;
+    // the first candidate: forward e[cnt], backward e[cnt - 1], when in range
+    const int ci = forward ? int(cnt) : int(cnt) - 1;
+#pragma unroll
+    for (int k = 0; k < kLinearTail; k++)
+      if (k == ci && uint32_t(k) < len) {
+        r.kidx = r.first + k;
+        r.kval = e[k];
+      }
+    r.first += cnt;
   }
   return r;
 }

@@ -56,7 +56,7 @@ def main():
     def f(r, k):
         try:
             return float(r[ix[k]])
-        except (KeyError, ValueError):
+        except (KeyError, ValueError, IndexError):
             return 0.0
     tot = sum(f(r, "Warp Stall Sampling (All Samples)") for r in data) or 1.0
     stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
