@@ -436,6 +436,13 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n; b0 += gridDim.x * blockDim.x) {
     const uint32_t i = b0 + threadIdx.x;
+    {  // next iteration's query stream into L2 while this one waits on the structure
+      const uint32_t nx = i + gridDim.x * blockDim.x;
+      if (nx < n && (threadIdx.x & 31) < 3) {
+        const T* base = (threadIdx.x & 31) == 0 ? qx : ((threadIdx.x & 31) == 1 ? qy : qt);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (nx & ~31u)));
+      }
+    }
     bool defer = false;
     WalkRecord rec;
     if (i < n) {
@@ -553,6 +560,14 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
   const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (unsigned b0 = blockIdx.x * blockDim.x; b0 < m; b0 += gridDim.x * blockDim.x) {
     const unsigned k = b0 + threadIdx.x;
+    {  // next iteration's record into L2
+      const unsigned nk = k + gridDim.x * blockDim.x;
+      if (nk < m) {
+        const char* rp = CONT ? reinterpret_cast<const char*>(static_cast<const ContRecord*>(in) + nk)
+                              : reinterpret_cast<const char*>(static_cast<const WalkRecord*>(in) + nk);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+      }
+    }
     bool defer = false;
     float fx = 0.f, fy = 0.f, ft = 0.f;
     uint32_t qi = 0;
