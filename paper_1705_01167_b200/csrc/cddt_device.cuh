@@ -491,6 +491,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
 struct WalkDefer {
   uint32_t lo, n;  // CSR row of the query
   int idx;         // candidate whose window walk is pending; -1: near field
+  float cval;      // its zero point (phase 1 loaded it)
 };
 
 __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x, double y, int a,
@@ -510,6 +511,7 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
   def->n = q.hi - q.lo;
   if (!((w0.y >> (cxi & 31)) & 1u)) {
     def->idx = -1;  // near field needs the walker: phase 2 redoes the whole query
+    def->cval = 0.f;
     return false;
   }
   const RowSearch rs =
@@ -519,7 +521,8 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
   const double4 dir = c.dirs[a];
   for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
        idx += step) {
-    const double vv = (double)(uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx));
+    const float fv = uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx);
+    const double vv = (double)fv;
     const double d = q.forward ? vv - q.xq : q.xq - vv;
     if (d >= c.max_range) break;
     int32_t cell;
@@ -528,6 +531,7 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
       return true;
     }
     def->idx = idx;  // first verification window: hand over to phase 2
+    def->cval = fv;
     return false;
   }
   *result = c.max_range;
@@ -546,6 +550,7 @@ struct WinState {
   int idx;         // next candidate
   int cx, cy;      // walker cell and entry parameter (continuations)
   double t;
+  float cval;      // FRESH: the zero point of candidate idx, from phase 1
 };
 
 // FRESH: s.idx is phase 1's candidate (landing probe done, no walker yet);
@@ -564,7 +569,7 @@ __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, doub
   Walker<true> wk;
   int idx = s.idx, windows = 0;
   if (FRESH) {
-    const double vv = (double)__ldg(v + idx);
+    const double vv = (double)s.cval;
     const double d = forward ? vv - xq : xq - vv;
     *result = c.max_range;
     if (d >= c.max_range) return true;
@@ -610,7 +615,7 @@ __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, doub
 
 __device__ __forceinline__ double directional_cast_resume(const CddtView& c, double x, double y,
                                                           int a, const WalkDefer& def) {
-  WinState s{def.lo, def.n, def.idx, 0, 0, 0.0};
+  WinState s{def.lo, def.n, def.idx, 0, 0, 0.0, __ldg(c.zp + def.lo + def.idx)};
   double r;
   resume_windows<true>(c, x, y, a, s, 0x7fffffff, &r);
   return r;

@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
         rec.lo = def.lo;
         rec.n = def.n;
         rec.idx = def.idx;
-        rec.pad = 0;
+        rec.pad = __float_as_int(def.cval);  // windows: the candidate's zero point
       }
     }
     const bool near = defer && rec.idx < 0, win = defer && !near;
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         qi = __float_as_uint(w0.w);
         s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z),
                      __float_as_int(w1.w), __float_as_int(w2.x),
-                     __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z))};
+                     __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z)), 0.f};
       } else {
         const float4* src = reinterpret_cast<const float4*>(static_cast<const WalkRecord*>(in) + k);
         const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1);
@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         fy = w0.y;
         ft = w0.z;
         qi = __float_as_uint(w0.w);
-        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z), 0, 0, 0.0};
+        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z), 0, 0, 0.0,
+                     w1.w};
       }
       a = direction_index(normalize_angle_2pi(double(ft)), c.K);
       double res;
