@@ -2,8 +2,8 @@
 rangelib/mcl.hpp:101-127, proj/src/mcl.cpp:156-201) with particles resident in
 HBM and every per-particle loop a kernel of librl_cddt.so.
 
-Single GPU: one C-ABI call per step (rl_mcl_step). Across GPUs (an initialised
-torch.distributed group with world_size > 1): particles are sharded, the map
+Single GPU: one C-ABI call per step (rl_mcl_step). Across GPUs (Mcl(...,
+group=<torch.distributed process group>) with world_size > 1): particles are sharded, the map
 and CDDT are replicated on every GPU, and the step runs stage by stage with two
 exchanges over NCCL — the weight-sum all-reduce (max log-weight, then the
 normalising sum and pose moments) and the resampling all-gather of
@@ -84,9 +84,12 @@ class Mcl:
         self.table, self.inv_res = table, inv_res
         self.zdim = 0 if table is None else int(table.shape[0])
         self.dev = device if device is not None else torch.device("cuda", self.cddt.info().device)
+        # sharded only when given a process group: a process that merely has
+        # torch.distributed initialised (e.g. a multi-rank benchmark) keeps a
+        # whole filter of its own
         self.world, self.rank = 1, 0
         self.group = group
-        if dist.is_available() and dist.is_initialized():
+        if group is not None:
             self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         n = cfg.particle_count
         if n % self.world:

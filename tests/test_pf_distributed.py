@@ -102,7 +102,8 @@ def _run(rank, world, port, q):
         cfg = mcl.MclConfig(particle_count=N, seed=11)
         cfg.motion = mcl.MotionNoise(1.0, 0.0, 0.0, 0.02)
         cfg.beam.z_max = 120.0
-        m = mcl.Mcl(_Method(120.0), cfg, device=torch.device("cpu"), stages=None)
+        m = mcl.Mcl(_Method(120.0), cfg, device=torch.device("cpu"), stages=None,
+                    group=dist.group.WORLD)
         m.stages = HostStages(m, orc, scan, params)
         px, py, pt = synth.particles(x, y, t, N, 6.0, 0.1, seed=5)
         m.set_particles(px, py, pt)
