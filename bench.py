@@ -415,7 +415,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                     "d2h_bytes_per_step": 4 * n, "steps": args.e2e_steps,
                     "path": "rl_cddt_cast_batch_host (pinned host buffers, 3-stream pipeline)"},
-            # per step: k_cast_defer_p1, four k_walk_pass window passes, k_cast_defer_p2<near>
+            # per step: k_cast_defer_p1, four k_walk_pass window passes, k_cast_near
             "gpu_launches": 6 * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -423,7 +423,7 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_query": bytes_per_query, "sectors_per_query": s_bar,
                          "sector_sample": ns,
                          "kernel": "batched cast = k_cast_defer_p1 + 4 x k_walk_pass (window "
-                                   "passes) + k_cast_defer_p2<near> back to back; timed per step"},
+                                   "passes) + k_cast_near back to back; timed per step"},
             "cpu_baseline": {"value": sample / ref_dt, "unit": UNIT, "cores": threads,
                              "kind": "reference",
                              "sample": f"{sample} queries of this workload on {how}; "

@@ -108,7 +108,7 @@ __device__ __forceinline__ bool occupied(const CddtView& c, int x, int y) {
 // per-query constants (step, bias 1.0/0.0, axis-parallel flag) and computes
 // both next boundaries with selects, so lanes walking in different directions
 // do not diverge. It costs registers and one extra division per step: it pays
-// in the dedicated walk kernel (k_cast_defer_p2, every lane walking) and not
+// in the dedicated walk kernels (k_walk_pass, every lane walking) and not
 // in the monolithic kernels, which use the branchy form.
 template <bool kBranchFree>
 struct Walker {
@@ -613,12 +613,5 @@ __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, doub
   return true;
 }
 
-__device__ __forceinline__ double directional_cast_resume(const CddtView& c, double x, double y,
-                                                          int a, const WalkDefer& def) {
-  WinState s{def.lo, def.n, def.idx, 0, 0, 0.0, __ldg(c.zp + def.lo + def.idx)};
-  double r;
-  resume_windows<true>(c, x, y, a, s, 0x7fffffff, &r);
-  return r;
-}
 
 }  // namespace rl

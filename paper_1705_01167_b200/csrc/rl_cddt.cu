@@ -398,9 +398,9 @@ __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict
 // Phase 1 settles every query that needs no walker with uniform control flow
 // and queues the rest — with the CSR row and the pending candidate — through
 // a per-CTA shared-memory compaction (one global atomic per CTA iteration).
-// Phase 2 resumes exactly there (cddt_device.cuh directional_cast_resume),
-// with every lane walking; near-field queries are redone in full by a third
-// launch. Records are streamed evict-first past L2.
+// The window passes (k_walk_pass) resume exactly there, every lane walking;
+// near-field queries are redone in full by k_cast_near. Records are streamed
+// evict-first past L2.
 struct __align__(16) WalkRecord {
   float x, y, t;
   uint32_t i, lo, n;
@@ -494,32 +494,20 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
   }
 }
 
-// Near-field records, redone in full (NEAR), or (legacy single pass) the
-// pending verification windows resumed to completion.
-template <class T, bool NEAR>
-__global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_defer_p2(CddtView c,
-                                                          const WalkRecord* __restrict__ q,
-                                                          const unsigned* __restrict__ qn,
-                                                          uint32_t n, T* __restrict__ out) {
-  const unsigned m = qn[NEAR ? 1 : 0];
+// Near-field records (origin not clear), redone in full.
+template <class T>
+__global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_near(CddtView c,
+                                                      const WalkRecord* __restrict__ q,
+                                                      const unsigned* __restrict__ qn,
+                                                      uint32_t n, T* __restrict__ out) {
+  const unsigned m = qn[1];
   for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
-    WalkRecord r;
-    {
-      const float4* src = reinterpret_cast<const float4*>(q + (NEAR ? n - 1 - k : k));
-      float4* dst = reinterpret_cast<float4*>(&r);
-      dst[0] = __ldcs(src);
-      dst[1] = __ldcs(src + 1);
-    }
-    const double x = double(r.x), y = double(r.y);
-    const int a = direction_index(normalize_angle_2pi(double(r.t)), c.K);
-    double res;
-    if (NEAR) {
-      CastOut o;
-      res = directional_cast(c, x, y, a, o);
-    } else {
-      res = directional_cast_resume(c, x, y, a, WalkDefer{r.lo, r.n, r.idx});
-    }
-    __stcs(out + r.i, T(res));
+    const float4* src = reinterpret_cast<const float4*>(q + (n - 1 - k));
+    const float4 w0 = __ldcs(src);  // x, y, theta, query index
+    const int a = direction_index(normalize_angle_2pi(double(w0.z)), c.K);
+    CastOut o;
+    const double res = directional_cast(c, double(w0.x), double(w0.y), a, o);
+    __stcs(out + __float_as_uint(w0.w), T(res));
   }
 }
 
@@ -712,7 +700,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     static const int pw0 = walk_ctas(k_walk_pass<T, false, false>);
     static const int pwc = walk_ctas(k_walk_pass<T, true, false>);
     static const int pwl = walk_ctas(k_walk_pass<T, true, true>);
-    static const int pn = resident_ctas(k_cast_defer_p2<T, true>);
+    static const int pn = resident_ctas(k_cast_near<T>);
     RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(
         1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
@@ -729,7 +717,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     k_walk_pass<T, true, true><<<sm_count() * pwl, kWalkThreads, 0, st>>>(
         v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
         nullptr, 0, out);
-    k_cast_defer_p2<T, true><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
+    k_cast_near<T><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
 #ifdef RL_DEBUG_COUNTS
     {
       unsigned h[2 + kPasses];
