@@ -616,3 +616,32 @@ def test_window_pass_queues(cap):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().endswith("EQUAL"), r.stdout + r.stderr[-2000:]
+
+
+def test_casts_after_every_structure_change(rl, synth):
+    """Queries read derived per-row records (CSR range + search probes) that
+    must be rebuilt after edits, prune and snapshot loads: after each change
+    the batched casts (split path, >= 4M queries, and the single f64 kernel)
+    equal those of a structure built fresh from the same grid."""
+    import torch
+    g = synth.maze_map(400, 400, 0.10, 6)
+    K, mr = 108, 250.0
+    q = [dev(a) for a in synth.free_queries(g, 1 << 22, seed=41)]
+    q64 = [t.double() for t in q]
+
+    def same(a, b):
+        ra, rb = a.cast_batch(*q), b.cast_batch(*q)
+        fa, fb = a.cast_batch_f64(*q64), b.cast_batch_f64(*q64)
+        torch.cuda.synchronize()
+        assert torch.equal(ra, rb) and torch.equal(fa, fb)
+
+    gpu = make_gpu(rl, g, K, mr)
+    for rnd in range(3):
+        xy, occ = synth.block_edits(400, 400, 60, seed=700 + rnd)
+        gpu.set_occupancy_batch(xy, occ)
+    edited = gpu.export()["grid"]
+    same(gpu, make_gpu(rl, edited, K, mr))
+    gpu.prune()
+    pruned = make_gpu(rl, edited, K, mr, prune=True)
+    same(gpu, pruned)
+    same(rl.deserialize_cddt(rl.serialize_cddt(gpu)), pruned)
