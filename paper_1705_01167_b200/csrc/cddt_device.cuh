@@ -614,4 +614,43 @@ __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, doub
 }
 
 
+// Near-field records (origin not clear): the near-field walk, the row search
+// and the candidate loop up to the first verification window. A query that
+// needs one leaves with the candidate loop's state (the walker exists), for
+// resume_windows<false>; its landing probe is repeated there (same answer).
+// Phase 1 already established the origin is in bounds and unoccupied.
+__device__ __forceinline__ bool near_cast_p1(const CddtView& c, double x, double y, int a,
+                                             double* result, WinState* s) {
+  const QueryRow q = query_row(c, x, y, a);
+  const double4 dir = c.dirs[a];
+  Walker<true> wk;
+  wk.init_at(x, y, dir, 0.0);
+  const double r = wk.scan_to(c, kNearField);  // cddt.cpp:225-232
+  if (r >= 0.0) {
+    *result = (c.max_range < r) ? c.max_range : r;
+    return true;
+  }
+  *result = c.max_range;
+  if (r == kWalkExit) return true;
+  const RowSearch rs =
+      partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint, q.hint2);
+  const int n = (int)(q.hi - q.lo);
+  const int step = q.forward ? 1 : -1;
+  for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
+       idx += step) {
+    const double vv =
+        (double)(uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx));
+    const double d = q.forward ? vv - q.xq : q.xq - vv;
+    if (d >= c.max_range) break;
+    int32_t cell;
+    if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {
+      *result = d;
+      return true;
+    }
+    *s = WinState{q.lo, uint32_t(n), idx, wk.cx, wk.cy, wk.t, 0.f};
+    return false;
+  }
+  return true;
+}
+
 }  // namespace rl

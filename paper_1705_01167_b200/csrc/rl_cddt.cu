@@ -494,23 +494,6 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
   }
 }
 
-// Near-field records (origin not clear), redone in full.
-template <class T>
-__global__ void __launch_bounds__(256, RL_P2_CTAS) k_cast_near(CddtView c,
-                                                      const WalkRecord* __restrict__ q,
-                                                      const unsigned* __restrict__ qn,
-                                                      uint32_t n, T* __restrict__ out) {
-  const unsigned m = qn[1];
-  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
-    const float4* src = reinterpret_cast<const float4*>(q + (n - 1 - k));
-    const float4 w0 = __ldcs(src);  // x, y, theta, query index
-    const int a = direction_index(normalize_angle_2pi(double(w0.z)), c.K);
-    CastOut o;
-    const double res = directional_cast(c, double(w0.x), double(w0.y), a, o);
-    __stcs(out + __float_as_uint(w0.w), T(res));
-  }
-}
-
 // Window passes. A query needing many verification windows (a ray grazing a
 // wall meets one failing candidate per wall cell) holds its whole warp in a
 // single resume-to-completion pass; instead, pass k scans at most cap_k
@@ -621,6 +604,64 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
   }
 }
 
+// Near-field records (origin not clear): near-field walk, search and landing
+// probes here; queries that need a verification window join the window
+// passes as continuations (queue A, after pass 0's own).
+template <class T>
+__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_cast_near(
+    CddtView c, const WalkRecord* __restrict__ q, const unsigned* __restrict__ qn, uint32_t n,
+    ContRecord* __restrict__ oq, unsigned* __restrict__ out_count, uint32_t out_cap,
+    T* __restrict__ out) {
+  __shared__ unsigned cnt_s[kWalkThreads / 32], base_s;
+  const unsigned m = qn[1];
+  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (unsigned b0 = blockIdx.x * blockDim.x; b0 < m; b0 += gridDim.x * blockDim.x) {
+    const unsigned k = b0 + threadIdx.x;
+    bool defer = false;
+    float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    WinState s{};
+    int a = 0;
+    if (k < m) {
+      w0 = __ldcs(reinterpret_cast<const float4*>(q + (n - 1 - k)));  // x, y, theta, index
+      a = direction_index(normalize_angle_2pi(double(w0.z)), c.K);
+      double res;
+      if (near_cast_p1(c, double(w0.x), double(w0.y), a, &res, &s))
+        __stcs(out + __float_as_uint(w0.w), T(res));
+      else
+        defer = true;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, defer);
+    if (lane == 0) cnt_s[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < kWalkThreads / 32; w++) {
+        const unsigned x = cnt_s[w];
+        cnt_s[w] = tot;
+        tot += x;
+      }
+      base_s = tot ? atomicAdd(out_count, tot) : 0u;
+    }
+    __syncthreads();
+    if (defer) {
+      const unsigned slot = base_s + cnt_s[wid] + __popc(bal & ((1u << lane) - 1));
+      if (slot < out_cap) {
+        float4* dst = reinterpret_cast<float4*>(oq + slot);
+        __stcs(dst, w0);
+        __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
+                                    __int_as_float(s.idx), __int_as_float(s.cx)));
+        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
+                                    __int_as_float(__double2loint(s.t)),
+                                    __int_as_float(__double2hiint(s.t))));
+      } else {  // queue full: finish here
+        __stcs(out + __float_as_uint(w0.w),
+               T(finish_windows(c, double(w0.x), double(w0.y), a, s)));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // CTAs per SM for a kernel at 256 threads (one full wave, no partial tail).
 template <class K>
 static int resident_ctas(K kernel) {
@@ -700,11 +741,13 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     static const int pw0 = walk_ctas(k_walk_pass<T, false, false>);
     static const int pwc = walk_ctas(k_walk_pass<T, true, false>);
     static const int pwl = walk_ctas(k_walk_pass<T, true, true>);
-    static const int pn = resident_ctas(k_cast_near<T>);
+    static const int pn = walk_ctas(k_cast_near<T>);
     RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(
         1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), kP1Threads, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
+    k_cast_near<T><<<sm_count() * pn, kWalkThreads, 0, st>>>(v, q, qn, uint32_t(n), qa, qn + 2,
+                                                             uint32_t(cap_a), out);
     k_walk_pass<T, false, false><<<sm_count() * pw0, kWalkThreads, 0, st>>>(
         v, q, qn, uint32_t(n), kCaps[0], qa, qn + 2, uint32_t(cap_a), out);
     for (int p = 1; p < kPasses; p++) {  // queue p-1 -> queue p (A, B, A, ...)
@@ -717,7 +760,6 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     k_walk_pass<T, true, true><<<sm_count() * pwl, kWalkThreads, 0, st>>>(
         v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
         nullptr, 0, out);
-    k_cast_near<T><<<sm_count() * pn, 256, 0, st>>>(v, q, qn, uint32_t(n), out);
 #ifdef RL_DEBUG_COUNTS
     {
       unsigned h[2 + kPasses];
