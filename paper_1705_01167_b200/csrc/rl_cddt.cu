@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict
     CastOut o;
     const double r = directional_cast(c, x, y, direction_index(th, c.K), o);
     if (out) __stcs(out + i, T(r));
-    if (HIT) hit[i] = o.hit;
+    if (HIT && hit) hit[i] = o.hit;
     if (RES) {
       if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
       if (res_idx) res_idx[i] = o.res_idx;

@@ -645,3 +645,26 @@ def test_casts_after_every_structure_change(rl, synth):
     pruned = make_gpu(rl, edited, K, mr, prune=True)
     same(gpu, pruned)
     same(rl.deserialize_cddt(rl.serialize_cddt(gpu)), pruned)
+
+
+def test_f64_batch_optional_outputs(rl, synth):
+    """Every optional output of rl_cddt_cast_batch_f64 (range, hit cell,
+    resolving row/index) may be omitted independently."""
+    import itertools
+    import torch
+    g = synth.rect_map(300, 200, 20, seed=3)
+    gpu = make_gpu(rl, g, 72, 150.0)
+    q = [dev(a.astype(np.float64)) for a in synth.free_queries(g, 50_000, seed=5)]
+    n = q[0].numel()
+    full = dict(out=torch.empty(n, dtype=torch.float64, device="cuda"),
+                hit=torch.empty(n, dtype=torch.int32, device="cuda"),
+                res_row=torch.empty(n, dtype=torch.int64, device="cuda"),
+                res_idx=torch.empty(n, dtype=torch.int32, device="cuda"))
+    gpu.cast_batch_f64(*q, **full)
+    torch.cuda.synchronize()
+    for mask in itertools.product((0, 1), repeat=4):
+        part = {k: torch.full_like(v, -7) for (k, v), m in zip(full.items(), mask) if m}
+        gpu.cast_batch_f64(*q, **{k: part.get(k) for k in full})
+        torch.cuda.synchronize()
+        for k, v in part.items():
+            assert torch.equal(v, full[k]), (mask, k)
