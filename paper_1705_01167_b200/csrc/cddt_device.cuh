@@ -303,7 +303,11 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
                                                             uint32_t n, double xq, bool forward,
                                                             float4 h, float4 h2) {
   RowSearch r{0, ~0u, 0.f};
-  const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
+  // one strict threshold for both directions: for a float e,
+  //   e <= RD_f32(xq)  <=>  e < nextup(RD_f32(xq))      (forward)
+  //   e <  RU_f32(xq)                                    (backward)
+  const float thr = forward ? nextafterf(__double2float_rd(xq), __int_as_float(0x7f800000))
+                            : __double2float_ru(xq);
   uint32_t len = n, path = 0;
 #pragma unroll
   for (int l = 0; l < kHintLevels; l++) {
@@ -317,7 +321,7 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
     } else {
       e = path == 0 ? h2.y : path == 1 ? h2.z : path == 2 ? h2.w : __ldg(v + mid);
     }
-    const bool pass = forward ? (e <= xlo) : (e < xhi);
+    const bool pass = e < thr;
     if (pass != forward) {
       r.kidx = mid;
       r.kval = e;
@@ -333,7 +337,7 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
   while (len > kLinearTail) {
     const uint32_t half = len >> 1, mid = r.first + half;
     const float e = __ldg(v + mid);
-    const bool pass = forward ? (e <= xlo) : (e < xhi);
+    const bool pass = e < thr;
     if (pass != forward) {
       r.kidx = mid;
       r.kval = e;
@@ -347,22 +351,24 @@ __device__ __forceinline__ RowSearch partition_point_hinted(const float* __restr
   }
   if (kLinearTail > 0 && len > 0) {
     // the last <= kLinearTail elements in one round trip: the partition point
-    // is the count of passing elements (the predicate is monotone)
+    // is the count of passing elements (the predicate is monotone); slots
+    // past the row hold +inf, which never passes
     float e[kLinearTail > 0 ? kLinearTail : 1];
-#pragma unroll
-    for (int k = 0; k < kLinearTail; k++) e[k] = uint32_t(k) < len ? __ldg(v + r.first + k) : 0.f;
     uint32_t cnt = 0;
 #pragma unroll
-    for (int k = 0; k < kLinearTail; k++)
-      cnt += (uint32_t(k) < len && (forward ? (e[k] <= xlo) : (e[k] < xhi))) ? 1u : 0u;
+    for (int k = 0; k < kLinearTail; k++) {
+      e[k] = uint32_t(k) < len ? __ldg(v + r.first + k) : __int_as_float(0x7f800000);
+      cnt += e[k] < thr ? 1u : 0u;
+    }
     // the first candidate: forward e[cnt], backward e[cnt - 1], when in range
     const int ci = forward ? int(cnt) : int(cnt) - 1;
+    float cv = e[0];
 #pragma unroll
-    for (int k = 0; k < kLinearTail; k++)
-      if (k == ci && uint32_t(k) < len) {
-        r.kidx = r.first + k;
-        r.kval = e[k];
-      }
+    for (int k = 1; k < kLinearTail; k++) cv = ci == k ? e[k] : cv;
+    if (ci >= 0 && uint32_t(ci) < len) {
+      r.kidx = r.first + uint32_t(ci);
+      r.kval = cv;
+    }
     r.first += cnt;
   }
   return r;
