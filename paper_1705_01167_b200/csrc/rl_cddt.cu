@@ -1102,7 +1102,7 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
   constexpr int NSTREAM = 3;
-  const size_t chunk = std::min<size_t>(n, size_t(1) << 22);  // 4M queries = 64 MB per chunk
+  const size_t chunk = std::min<size_t>(n, size_t(1) << 23);  // 8M queries = 128 MB per chunk
   struct Lane {
     cudaStream_t s = nullptr;
     DevBuf<float> buf;  // x | y | theta | out
