@@ -84,10 +84,38 @@ __global__ void k_new_len(const uint32_t* __restrict__ off, const int32_t* __res
     len[g] = g < rows ? (off[g + 1] - off[g]) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]) : 0u;
 }
 
-// One warp per row. Unaffected rows: coalesced copy. Affected rows: lane 0
-// merges the old row with the row's sorted deltas (ZeroPointBin::insert /
-// remove_one semantics, cddt.hpp:67-84: removing takes out one element equal
-// to the value; equal keys are bit-identical so their order is immaterial).
+__device__ __forceinline__ float key2f(unsigned long long key) {
+  const uint32_t k = uint32_t(key);
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// first index in v[0, n) whose value is > x (upper) or >= x (lower)
+__device__ __forceinline__ uint32_t row_bound(const float* __restrict__ v, uint32_t n, float x,
+                                              bool upper) {
+  uint32_t lo = 0, len = n;
+  while (len > 0) {
+    const uint32_t half = len >> 1, mid = lo + half;
+    const float e = v[mid];
+    if (upper ? !(x < e) : (e < x)) {
+      lo = mid + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  return lo;
+}
+
+// Merge each row's sorted delta records into its zero points, one warp per
+// row (Cddt::add/remove_pixel_points: insert keeps the row sorted, remove
+// drops one equal element; cddt.cpp:332-377, cddt.hpp:67-84). Equal values are
+// identical floats, so the merged row is the sorted multiset
+//   old - removed copies + added values,
+// which a warp builds in parallel for rows with at most 32 records: every
+// remove claims the next unclaimed copy of its value; a kept old element
+// lands at (its index - removed before it + adds smaller than it); an add
+// lands after the kept copies <= its value and the adds before it. Rows with
+// more records fall back to a sequential merge by lane 0.
 __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* __restrict__ old_zp,
                              const uint32_t* __restrict__ new_off, float* __restrict__ new_zp,
                              const int32_t* __restrict__ add_cnt,
@@ -96,36 +124,85 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
                              const int8_t* __restrict__ vals, unsigned n_rec, size_t rows,
                              unsigned* __restrict__ unmatched) {
   const unsigned lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
   const size_t warp = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
   const size_t nwarps = (size_t(gridDim.x) * blockDim.x) >> 5;
   for (size_t g = warp; g < rows; g += nwarps) {
     const uint32_t a = old_off[g], b = old_off[g + 1];
     const uint32_t o = new_off[g];
-    if (add_cnt[g] == 0 && rem_cnt[g] == 0) {
+    const unsigned nd = unsigned(add_cnt[g] + rem_cnt[g]);
+    if (nd == 0) {
       for (uint32_t i = a + lane; i < b; i += 32) new_zp[o + (i - a)] = old_zp[i];
       continue;
     }
-    if (lane != 0) continue;
-    // delta range of row g: lower_bound of g<<32 in the sorted keys
-    const unsigned long long lo_key = static_cast<unsigned long long>(g) << 32;
-    unsigned lo = 0, len = n_rec;
-    while (len > 0) {
-      unsigned half = len >> 1, mid = lo + half;
-      if (keys[mid] < lo_key) {
-        lo = mid + 1;
-        len -= half + 1;
-      } else {
-        len = half;
+    // delta range of row g: lower_bound of g<<32 in the sorted keys (lane 0)
+    unsigned j0 = 0;
+    if (lane == 0) {
+      const unsigned long long lo_key = static_cast<unsigned long long>(g) << 32;
+      unsigned lo = 0, len = n_rec;
+      while (len > 0) {
+        const unsigned half = len >> 1, mid = lo + half;
+        if (keys[mid] < lo_key) {
+          lo = mid + 1;
+          len -= half + 1;
+        } else {
+          len = half;
+        }
       }
+      j0 = lo;
     }
-    unsigned j = lo;
-    const unsigned jend = lo + unsigned(add_cnt[g] + rem_cnt[g]);
+    j0 = __shfl_sync(0xffffffffu, j0, 0);
+    const float* __restrict__ row = old_zp + a;
+    const uint32_t n = b - a;
+    if (nd <= 32) {
+      const bool has = lane < nd;
+      const float dv = has ? key2f(keys[j0 + lane]) : 0.f;
+      const bool add = has && vals[j0 + lane] > 0, rem = has && !add;
+      const unsigned add_mask = __ballot_sync(0xffffffffu, add);
+      const unsigned rem_mask = __ballot_sync(0xffffffffu, rem);
+      // removes: the k-th remove of value v drops old copy lower_bound(v) + k
+      const unsigned same = __match_any_sync(0xffffffffu, __float_as_uint(dv)) & rem_mask;
+      uint32_t ridx = 0xffffffffu;
+      if (rem) {
+        const uint32_t p = row_bound(row, n, dv, false) + __popc(same & lt);
+        if (p < n && row[p] == dv)
+          ridx = p;
+        else
+          atomicAdd(unmatched, 1u);
+      }
+      // adds: after the kept copies <= dv and the adds sorted before this one
+      unsigned rem_le = 0;  // removed copies with value <= dv
+      for (unsigned l = 0; l < nd; l++) {
+        const float dl = __shfl_sync(0xffffffffu, dv, l);
+        rem_le += ((rem_mask >> l) & 1u) && !(dv < dl) ? 1u : 0u;
+      }
+      if (add) new_zp[o + row_bound(row, n, dv, true) - rem_le + __popc(add_mask & lt)] = dv;
+      // kept old elements, 32 at a time
+      for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const float e = i < n ? row[i] : 0.f;
+        bool removed = false;
+        unsigned rb = 0, adds_lt = 0;
+        for (unsigned l = 0; l < nd; l++) {
+          const uint32_t rl = __shfl_sync(0xffffffffu, ridx, l);
+          const float dl = __shfl_sync(0xffffffffu, dv, l);
+          removed |= rl == i;
+          rb += rl < i ? 1u : 0u;
+          adds_lt += ((add_mask >> l) & 1u) && dl < e ? 1u : 0u;
+        }
+        if (i < n && !removed) new_zp[o + i - rb + adds_lt] = e;
+      }
+      continue;
+    }
+    if (lane != 0) continue;
+    // sequential merge for rows with many records
+    unsigned j = j0;
+    const unsigned jend = j0 + nd;
     uint32_t i = a, w = o;
     unsigned miss = 0;
     while (i < b || j < jend) {
       if (j < jend) {
-        const float dv = __uint_as_float((keys[j] & 0x80000000ull) ? uint32_t(keys[j]) & 0x7fffffffu
-                                                                    : ~uint32_t(keys[j]));
+        const float dv = key2f(keys[j]);
         if (i == b || dv < old_zp[i]) {
           if (vals[j] > 0)
             new_zp[w++] = dv;
@@ -276,8 +353,12 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   k_delta_records<<<blocks_for(size_t(nd) * c->S, 256), 256, 0, st>>>(
       d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, keys, vals, d_count, add_cnt, rem_cnt);
   RL_CK(cudaGetLastError());
+  // keys are row<<32 | value; the unused slots (all ones) must sort last, so
+  // the sort covers the value bits and enough row bits that no row is all ones
+  int row_bits = 1;
+  while ((size_t(1) << row_bits) <= rows) row_bits++;
   RL_CK(cub::DeviceRadixSort::SortPairs(tmp, sort_tmp, keys, keys_sorted, vals, vals_sorted,
-                                        int(cap), 0, 64, st));
+                                        int(cap), 0, 32 + row_bits, st));
   // 4. new offsets and merge into the spare buffers, then swap
   if (c->off_spare.n < rows + 1) RL_TRY(c->off_spare.alloc(rows + 1));
   const size_t zp_need = c->zero_points + cap;
