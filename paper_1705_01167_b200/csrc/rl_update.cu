@@ -131,8 +131,18 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
     const uint32_t a = old_off[g], b = old_off[g + 1];
     const uint32_t o = new_off[g];
     const unsigned nd = unsigned(add_cnt[g] + rem_cnt[g]);
-    if (nd == 0) {
-      for (uint32_t i = a + lane; i < b; i += 32) new_zp[o + (i - a)] = old_zp[i];
+    if (nd == 0) {  // unchanged row: copy, four loads in flight per lane
+      uint32_t i = a + lane;
+      for (; i + 96 < b; i += 128) {
+        const float v0 = __ldcs(old_zp + i), v1 = __ldcs(old_zp + i + 32);
+        const float v2 = __ldcs(old_zp + i + 64), v3 = __ldcs(old_zp + i + 96);
+        float* d = new_zp + o + (i - a);
+        d[0] = v0;
+        d[32] = v1;
+        d[64] = v2;
+        d[96] = v3;
+      }
+      for (; i < b; i += 32) new_zp[o + (i - a)] = __ldcs(old_zp + i);
       continue;
     }
     // delta range of row g: lower_bound of g<<32 in the sorted keys (lane 0)
