@@ -15,10 +15,9 @@
 
 namespace rl {
 
-#ifndef RL_SENSOR_PB
-#define RL_SENSOR_PB 16
-#endif
-constexpr int kSensorParticlesPerCta = RL_SENSOR_PB;  // particles per CTA (<= 32)
+// particles per CTA: 16 for large sets (config 4), 8 below kSmallSet so a
+// few thousand particles still fill the GPU (config 2)
+constexpr size_t kSmallSet = 16384;
 
 struct BeamParams {
   double w_hit, w_short, w_max, w_rand, sigma_hit, lambda_short, z_max;
@@ -80,7 +79,7 @@ __device__ __forceinline__ double item_loglike(double e, int b, const double* __
 #ifndef RL_SENSOR_MINB
 #define RL_SENSOR_MINB 4  // resident CTAs per SM (caps registers at 64)
 #endif
-template <bool MOTION>
+template <bool MOTION, int kSensorParticlesPerCta>
 __global__ void __launch_bounds__(256, RL_SENSOR_MINB) k_sensor_logw(
     CddtView c, double* __restrict__ px, double* __restrict__ py, double* __restrict__ pt,
     size_t n, const double* __restrict__ scan, int nb, double fov, BeamParams bp,
@@ -176,21 +175,20 @@ int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
   if (params)
     bp = BeamParams{params->w_hit,     params->w_short,      params->w_max, params->w_rand,
                     params->sigma_hit, params->lambda_short, params->z_max};
-  const int ctas = int((n + kSensorParticlesPerCta - 1) / kSensorParticlesPerCta);
   const MotionArgs m = mot ? *mot : MotionArgs{};
-  const size_t smem = sizeof(double) * (kSensorParticlesPerCta + 1) * nb + sizeof(int) * nb;
-  if (mot) {
+  auto launch = [&](auto kernel, int pb) -> int {
+    const int ctas = int((n + pb - 1) / pb);
+    const size_t smem = sizeof(double) * (pb + 1) * nb + sizeof(int) * nb;
     if (smem > 48 * 1024)
-      RL_CK(cudaFuncSetAttribute(k_sensor_logw<true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_sensor_logw<true><<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp,
-                                                 table, zdim, inv_res, logw, m, gmax_key);
+      RL_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kernel<<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp, table, zdim,
+                                    inv_res, logw, m, gmax_key);
+    return RL_OK;
+  };
+  if (n < kSmallSet) {
+    RL_TRY(mot ? launch(k_sensor_logw<true, 8>, 8) : launch(k_sensor_logw<false, 8>, 8));
   } else {
-    if (smem > 48 * 1024)
-      RL_CK(cudaFuncSetAttribute(k_sensor_logw<false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_sensor_logw<false><<<ctas, 256, smem, st>>>(c->view(), px, py, pt, n, scan, nb, fov, bp,
-                                                  table, zdim, inv_res, logw, m, gmax_key);
+    RL_TRY(mot ? launch(k_sensor_logw<true, 16>, 16) : launch(k_sensor_logw<false, 16>, 16));
   }
   RL_CK(cudaGetLastError());
   return RL_OK;
