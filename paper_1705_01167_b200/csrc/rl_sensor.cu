@@ -6,6 +6,7 @@
 // in beam order 0..nbeams-1 — the reference's summation order, so the FP64
 // log-weight is reproducible. Normalisation (max-subtract, exp, sum, divide,
 // degenerate reset, mcl.cpp:108-119) follows as a reduction.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -14,6 +15,8 @@
 #include "rl_common.cuh"
 
 namespace rl {
+
+namespace cg = cooperative_groups;
 
 // particles per CTA: 16 for large sets (config 4), 8 below kSmallSet so a
 // few thousand particles still fill the GPU (config 2)
@@ -143,29 +146,55 @@ __global__ void __launch_bounds__(256, RL_SENSOR_MINB) k_sensor_logw(
   }
 }
 
-__global__ void k_exp_shift(const double* __restrict__ logw, const double* __restrict__ mx,
-                            double* __restrict__ w, size_t n) {
-  const double m = *mx;
+
+
+// sensor_update's normalisation (mcl.cpp:104-119) after the log-weights: one
+// cooperative launch. w = exp(logw - max) with the max from the atomic key,
+// per-block sums in a fixed tree, every block sums the block sums in the same
+// order, then w /= S (or 1/n and the degenerate flag when S is zero or not
+// finite).
+__global__ void __launch_bounds__(256) k_sensor_normalize(const double* __restrict__ logw,
+                                                          const unsigned long long* __restrict__ key,
+                                                          double* __restrict__ w, size_t n,
+                                                          double* __restrict__ partial,
+                                                          int* __restrict__ degenerate) {
+  cg::grid_group grid = cg::this_grid();
+  const double m = order_key_value(*key);
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double e = exp(logw[i] - m);
+    w[i] = e;
+    acc += e;
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int k = 0; k < 8; k++) b += red[k];
+    partial[blockIdx.x] = b;
+  }
+  grid.sync();
+  __shared__ double S_s;
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) v += __ldcg(partial + b);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) S_s = v;
+  }
+  __syncthreads();
+  const double S = S_s;
+  const bool bad = !(S > 0.0) || !isfinite(S);  // mcl.cpp:114
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
-    w[i] = exp(logw[i] - m);
+    w[i] = bad ? 1.0 / double(n) : __ldcg(w + i) / S;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *degenerate = bad ? 1 : 0;
 }
 
-__global__ void k_normalise(double* __restrict__ w, const double* __restrict__ sum, size_t n,
-                            int* __restrict__ degenerate) {
-  const double s = *sum;
-  const bool bad = !(s > 0.0) || !isfinite(s);  // mcl.cpp:114
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x)
-    w[i] = bad ? 1.0 / double(n) : w[i] / s;
-  if (bad && blockIdx.x == 0 && threadIdx.x == 0) *degenerate = 1;
-}
-
-static int blocks_for(size_t work, int threads) {
-  size_t b = (work + threads - 1) / threads;
-  size_t cap = size_t(sm_count()) * 16;
-  return int(std::max<size_t>(1, std::min(b, cap)));
-}
 
 int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
                        const double* scan, int nb, double fov, const rl_beam_params_t* params,
@@ -282,29 +311,34 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
-  // workspace: logw (if not given) | w (if not given) | max | sum | flag | cub temp
-  size_t cub_bytes = 0, cub2 = 0;
-  cub::DeviceReduce::Max(nullptr, cub_bytes, (double*)nullptr, (double*)nullptr, int(n), st);
-  cub::DeviceReduce::Sum(nullptr, cub2, (double*)nullptr, (double*)nullptr, int(n), st);
-  cub_bytes = std::max(cub_bytes, cub2);
-  const size_t need = 16 * n + 64 + cub_bytes + 256;
+  static const int coop = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sensor_normalize, 256, 0);
+    return per_sm;
+  }();
+  const int nblk = int(std::max<size_t>(
+      1, std::min((n + 255) / 256, size_t(sm_count()) * size_t(std::min(coop, 2)))));
+  // workspace: control {max key, flag} | logw (if not given) | w (if not given) | partials
+  const size_t need = 64 + 16 * n + 8 * size_t(nblk);
   if (c->ws.n < need) RL_TRY(c->ws.alloc(need));
   uint8_t* base = c->ws.p;
-  double* d_logw = logw ? logw : reinterpret_cast<double*>(base);
-  double* d_w = weight ? weight : reinterpret_cast<double*>(base + 8 * n);
-  double* d_max = reinterpret_cast<double*>(base + 16 * n);
-  double* d_sum = d_max + 1;
-  int* d_flag = reinterpret_cast<int*>(d_max + 2);
-  void* d_tmp = base + 16 * n + 64;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(base);
+  int* d_flag = reinterpret_cast<int*>(base + 8);
+  double* d_logw = logw ? logw : reinterpret_cast<double*>(base + 64);
+  double* d_w = weight ? weight : reinterpret_cast<double*>(base + 64 + 8 * n);
+  double* partial = reinterpret_cast<double*>(base + 64 + 16 * n);
+  RL_CK(cudaMemsetAsync(key, 0, 16, st));
   RL_TRY(sensor_logw_launch(c, const_cast<double*>(px), const_cast<double*>(py),
                             const_cast<double*>(pt), n, scan, nbeams, fov, params, table, zdim,
-                            inv_res, d_logw, nullptr, nullptr, st));
-  RL_CK(cub::DeviceReduce::Max(d_tmp, cub_bytes, d_logw, d_max, int(n), st));
-  k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(d_logw, d_max, d_w, n);
-  RL_CK(cub::DeviceReduce::Sum(d_tmp, cub_bytes, d_w, d_sum, int(n), st));
-  RL_CK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
-  k_normalise<<<blocks_for(n, 256), 256, 0, st>>>(d_w, d_sum, n, d_flag);
-  RL_CK(cudaGetLastError());
+                            inv_res, d_logw, nullptr, key, st));
+  if (coop < 1) {
+    set_error("sensor_update: normalisation kernel cannot be co-resident");
+    return RL_ECUDA;
+  }
+  size_t nn = n;
+  void* args[] = {&d_logw, &key, &d_w, &nn, &partial, &d_flag};
+  RL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sensor_normalize), dim3(nblk),
+                                    dim3(256), args, 0, st));
   int flag = 0;
   RL_CK(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
