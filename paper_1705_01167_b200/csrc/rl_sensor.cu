@@ -7,7 +7,6 @@
 // log-weight is reproducible. Normalisation (max-subtract, exp, sum, divide,
 // degenerate reset, mcl.cpp:108-119) follows as a reduction.
 #include <cooperative_groups.h>
-#include <cub/cub.cuh>
 
 #include <cmath>
 
