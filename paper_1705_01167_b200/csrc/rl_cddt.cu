@@ -678,7 +678,10 @@ static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t,
   k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
 }
 
-constexpr size_t kDeferMinQueries = size_t(1) << 22;
+#ifndef RL_DEFER_MIN_LOG2
+#define RL_DEFER_MIN_LOG2 22
+#endif
+constexpr size_t kDeferMinQueries = size_t(1) << RL_DEFER_MIN_LOG2;
 
 // Dispatch of the batched cast kernels for the device-pointer entry points.
 template <class T>
