@@ -521,6 +521,11 @@ def test_deferred_path_edge_cases(rl, oracle_mod):
     qy = rng.uniform(-3, 64, n).astype(np.float32)
     qt = rng.uniform(-40, 40, n).astype(np.float32)
     qx[: n // 8] = np.round(qx[: n // 8])  # exactly on lattice lines
+    # exactly on pixel-centre projections: ties between the query's projected
+    # x' and stored zero points along the axis-aligned slices
+    qx[n // 8: n // 4] = np.round(qx[n // 8: n // 4]) + 0.5
+    qy[n // 8: n // 4] = np.round(qy[n // 8: n // 4]) + 0.5
+    qt[n // 8: n // 4] = (np.pi / 2) * rng.integers(0, 4, n // 8)
     for K, mr in ((4, 0.0), (24, 0.5), (216, 2.0)):
         _deferred_vs_oracle(rl, oracle_mod, g, K, mr, qx, qy, qt)
 
