@@ -489,7 +489,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   return c.max_range;
 }
 
-// ---- split form for the deferred-walk batch kernels (rl_cddt.cu) ----
+// ---- split form for the deferred-walk batch kernels (rl_query.cu) ----
 // Phase 1 runs cddt.cpp:207-269 up to the first point where a RayWalker is
 // needed: a non-clear origin (near-field walk) or a candidate whose landing
 // probe does not settle it (verification window). Phase 2 resumes exactly

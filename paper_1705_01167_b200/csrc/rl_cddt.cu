@@ -1,5 +1,5 @@
-// CDDT / PCDDT construction, pruning and batched queries on sm_100a, behind
-// the C ABI in include/rl_cddt.h.
+// CDDT / PCDDT construction, pruning, handle lifecycle and export on sm_100a,
+// behind the C ABI in include/rl_cddt.h (queries: rl_query.cu).
 //
 // Device layout:
 //   flags[w*h]      u8  bit0 occupied, bit1 clear-3x3, bit2 membership
@@ -363,460 +363,6 @@ int build_structure(rl_cddt* c) {
 }
 
 // ---------------------------------------------------------------------------
-// K3: batched casts.
-//
-// Monolithic form (f64 / hit-cell / resolving-index outputs, and batches
-// below 4M queries): one thread per query, grid-stride, a single full wave
-// sized by the occupancy calculator (4 x 256-thread CTAs per SM at 64 regs).
-template <class T, class I, bool HIT, bool RES>
-__global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict__ qx,
-                                                 const T* __restrict__ qy,
-                                                 const T* __restrict__ qt, T* __restrict__ out,
-                                                 int32_t* __restrict__ hit,
-                                                 int64_t* __restrict__ res_row,
-                                                 int32_t* __restrict__ res_idx, I n) {
-  for (I i = I(blockIdx.x) * I(blockDim.x) + I(threadIdx.x); i < n;
-       i += I(gridDim.x) * I(blockDim.x)) {
-    // query streams are touched once: evict-first so the structure stays in L2
-    const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
-    const double th = normalize_angle_2pi(double(__ldcs(qt + i)));  // RayQuery ctor, raycast.hpp:47
-    CastOut o;
-    const double r = directional_cast(c, x, y, direction_index(th, c.K), o);
-    if (out) __stcs(out + i, T(r));
-    if (HIT && hit) hit[i] = o.hit;
-    if (RES) {
-      if (res_row) res_row[i] = o.res_idx >= 0 ? int64_t(o.res_g) : -1;
-      if (res_idx) res_idx[i] = o.res_idx;
-    }
-  }
-}
-
-// Deferred-walk form (f32 ranges only, >= 4M queries; the bench path).
-// About a third of the queries need a RayWalker (a near-field walk or a
-// verification window). Run inline, those walks execute with ~5 of 32 lanes
-// active and cost half the kernel time (profiles/r01/ncu_k_cast_v3.txt).
-// Phase 1 settles every query that needs no walker with uniform control flow
-// and queues the rest — with the CSR row and the pending candidate — through
-// a per-CTA shared-memory compaction (one global atomic per CTA iteration).
-// The window passes (k_walk_pass) resume exactly there, every lane walking;
-// near-field queries are redone in full by k_cast_near. Records are streamed
-// evict-first past L2.
-struct __align__(16) WalkRecord {
-  float x, y, t;
-  uint32_t i, lo, n;
-  int32_t idx, pad;
-};
-
-#ifndef RL_P1_CTAS
-#define RL_P1_CTAS 6  // resident CTAs per SM the register budget of phase 1 targets
-#endif
-#ifndef RL_P2_CTAS
-#define RL_P2_CTAS 4
-#endif
-#ifndef RL_WIN_CAPS
-#define RL_WIN_CAPS 1, 2, 4  // windows per query in each capped window pass; a last pass finishes
-#endif
-#ifndef RL_CONT_A_DIV
-#define RL_CONT_A_DIV 4  // continuation queue capacities: n / DIV records
-#endif
-#ifndef RL_CONT_B_DIV
-#define RL_CONT_B_DIV 16
-#endif
-#ifndef RL_P1_THREADS
-#define RL_P1_THREADS 64  // small CTAs: the per-iteration compaction barrier waits for fewer warps
-#endif
-constexpr int kP1Threads = RL_P1_THREADS, kP1Warps = kP1Threads / 32;
-template <class T>
-__global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_cast_defer_p1(
-    CddtView c, const T* __restrict__ qx, const T* __restrict__ qy, const T* __restrict__ qt,
-    T* __restrict__ out, uint32_t n, WalkRecord* __restrict__ q, unsigned* __restrict__ qn) {
-  // queue layout: window records grow up from q[0], near-field records down
-  // from q[n-1]; qn[0], qn[1] count them
-  __shared__ unsigned cnt_s[2][kP1Warps], base_s[2];
-  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n; b0 += gridDim.x * blockDim.x) {
-    const uint32_t i = b0 + threadIdx.x;
-    {  // next iteration's query stream into L2 while this one waits on the structure
-      const uint32_t nx = i + gridDim.x * blockDim.x;
-      if (nx < n && (threadIdx.x & 31) < 3) {
-        const T* base = (threadIdx.x & 31) == 0 ? qx : ((threadIdx.x & 31) == 1 ? qy : qt);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (nx & ~31u)));
-      }
-    }
-    bool defer = false;
-    WalkRecord rec;
-    if (i < n) {
-      rec.x = __ldcs(qx + i);
-      rec.y = __ldcs(qy + i);
-      rec.t = __ldcs(qt + i);
-      rec.i = i;
-      const double th = normalize_angle_2pi(double(rec.t));
-      double r;
-      WalkDefer def;
-      if (directional_cast_p1(c, double(rec.x), double(rec.y), direction_index(th, c.K), &r,
-                              &def)) {
-        __stcs(out + i, T(r));
-      } else {
-        defer = true;
-        rec.lo = def.lo;
-        rec.n = def.n;
-        rec.idx = def.idx;
-        rec.pad = __float_as_int(def.cval);  // windows: the candidate's zero point
-      }
-    }
-    const bool near = defer && rec.idx < 0, win = defer && !near;
-    const unsigned bw = __ballot_sync(0xffffffffu, win), bn = __ballot_sync(0xffffffffu, near);
-    if (lane == 0) {
-      cnt_s[0][wid] = __popc(bw);
-      cnt_s[1][wid] = __popc(bn);
-    }
-    __syncthreads();
-    if (threadIdx.x < 2) {
-      unsigned tot = 0;
-      for (int w = 0; w < kP1Warps; w++) {
-        const unsigned k = cnt_s[threadIdx.x][w];
-        cnt_s[threadIdx.x][w] = tot;
-        tot += k;
-      }
-      base_s[threadIdx.x] = tot ? atomicAdd(qn + threadIdx.x, tot) : 0u;
-    }
-    __syncthreads();
-    if (defer) {
-      const unsigned below = (1u << lane) - 1;
-      const size_t slot = win ? base_s[0] + cnt_s[0][wid] + __popc(bw & below)
-                              : n - 1 - (base_s[1] + cnt_s[1][wid] + __popc(bn & below));
-      const float4* src = reinterpret_cast<const float4*>(&rec);
-      float4* dst = reinterpret_cast<float4*>(q + slot);
-      __stcs(dst, src[0]);
-      __stcs(dst + 1, src[1]);
-    }
-    __syncthreads();
-  }
-}
-
-// Window passes. A query needing many verification windows (a ray grazing a
-// wall meets one failing candidate per wall cell) holds its whole warp in a
-// single resume-to-completion pass; instead, pass k scans at most cap_k
-// windows per query and queues the unfinished ones, with the candidate loop's
-// state, for pass k+1 (the last pass has no cap). Each pass is a full-width
-// walk over a shrinking queue.
-struct __align__(16) ContRecord {
-  float x, y, t;
-  uint32_t i, lo, n;
-  int32_t idx, cx, cy, pad;
-  double wt;
-};
-
-#ifndef RL_WALK_THREADS
-#define RL_WALK_THREADS 64  // small CTAs: cheap compaction barriers
-#endif
-constexpr int kWalkThreads = RL_WALK_THREADS;
-
-// out-of-line: the rare overflow path must not add to the pass's registers
-__device__ __noinline__ double finish_windows(const CddtView& c, double x, double y, int a,
-                                              WinState s) {
-  double res;
-  resume_windows<false>(c, x, y, a, s, 0x7fffffff, &res);
-  return res;
-}
-
-template <class T, bool CONT, bool LAST>
-__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_walk_pass(
-    CddtView c, const void* __restrict__ in, const unsigned* __restrict__ in_count,
-    uint32_t in_cap, int cap, ContRecord* __restrict__ oq, unsigned* __restrict__ out_count,
-    uint32_t out_cap, T* __restrict__ out) {
-  __shared__ unsigned cnt_s[kWalkThreads / 32], base_s;
-  // the producer counts every continuation, stored or (queue full) finished
-  const unsigned m = min(*in_count, in_cap);
-  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (unsigned b0 = blockIdx.x * blockDim.x; b0 < m; b0 += gridDim.x * blockDim.x) {
-    const unsigned k = b0 + threadIdx.x;
-    {  // next iteration's record into L2
-      const unsigned nk = k + gridDim.x * blockDim.x;
-      if (nk < m) {
-        const char* rp = CONT ? reinterpret_cast<const char*>(static_cast<const ContRecord*>(in) + nk)
-                              : reinterpret_cast<const char*>(static_cast<const WalkRecord*>(in) + nk);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
-      }
-    }
-    bool defer = false;
-    float fx = 0.f, fy = 0.f, ft = 0.f;
-    uint32_t qi = 0;
-    WinState s{};
-    int a = 0;
-    if (k < m) {
-      if (CONT) {
-        const float4* src = reinterpret_cast<const float4*>(static_cast<const ContRecord*>(in) + k);
-        const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1), w2 = __ldcs(src + 2);
-        fx = w0.x;
-        fy = w0.y;
-        ft = w0.z;
-        qi = __float_as_uint(w0.w);
-        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z),
-                     __float_as_int(w1.w), __float_as_int(w2.x),
-                     __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z)), 0.f};
-      } else {
-        const float4* src = reinterpret_cast<const float4*>(static_cast<const WalkRecord*>(in) + k);
-        const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1);
-        fx = w0.x;
-        fy = w0.y;
-        ft = w0.z;
-        qi = __float_as_uint(w0.w);
-        s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z), 0, 0, 0.0,
-                     w1.w};
-      }
-      a = direction_index(normalize_angle_2pi(double(ft)), c.K);
-      double res;
-      if (resume_windows<!CONT>(c, double(fx), double(fy), a, s, LAST ? 0x7fffffff : cap, &res))
-        __stcs(out + qi, T(res));
-      else
-        defer = true;
-    }
-    if (LAST) continue;
-    const unsigned bal = __ballot_sync(0xffffffffu, defer);
-    if (lane == 0) cnt_s[wid] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned tot = 0;
-      for (int w = 0; w < kWalkThreads / 32; w++) {
-        const unsigned q = cnt_s[w];
-        cnt_s[w] = tot;
-        tot += q;
-      }
-      base_s = tot ? atomicAdd(out_count, tot) : 0u;
-    }
-    __syncthreads();
-    if (defer) {
-      const unsigned slot = base_s + cnt_s[wid] + __popc(bal & ((1u << lane) - 1));
-      if (slot < out_cap) {  // ContRecord layout, as three 16-byte stores
-        float4* dst = reinterpret_cast<float4*>(oq + slot);
-        __stcs(dst, make_float4(fx, fy, ft, __uint_as_float(qi)));
-        __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
-                                    __int_as_float(s.idx), __int_as_float(s.cx)));
-        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
-                                    __int_as_float(__double2loint(s.t)),
-                                    __int_as_float(__double2hiint(s.t))));
-      } else {  // queue full: finish here
-        __stcs(out + qi, T(finish_windows(c, double(fx), double(fy), a, s)));
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Near-field records (origin not clear): near-field walk, search and landing
-// probes here; queries that need a verification window join the window
-// passes as continuations (queue A, after pass 0's own).
-template <class T>
-__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_cast_near(
-    CddtView c, const WalkRecord* __restrict__ q, const unsigned* __restrict__ qn, uint32_t n,
-    ContRecord* __restrict__ oq, unsigned* __restrict__ out_count, uint32_t out_cap,
-    T* __restrict__ out) {
-  __shared__ unsigned cnt_s[kWalkThreads / 32], base_s;
-  const unsigned m = qn[1];
-  const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (unsigned b0 = blockIdx.x * blockDim.x; b0 < m; b0 += gridDim.x * blockDim.x) {
-    const unsigned k = b0 + threadIdx.x;
-    bool defer = false;
-    float4 w0 = make_float4(0.f, 0.f, 0.f, 0.f);
-    WinState s{};
-    int a = 0;
-    if (k < m) {
-      w0 = __ldcs(reinterpret_cast<const float4*>(q + (n - 1 - k)));  // x, y, theta, index
-      a = direction_index(normalize_angle_2pi(double(w0.z)), c.K);
-      double res;
-      if (near_cast_p1(c, double(w0.x), double(w0.y), a, &res, &s))
-        __stcs(out + __float_as_uint(w0.w), T(res));
-      else
-        defer = true;
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, defer);
-    if (lane == 0) cnt_s[wid] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned tot = 0;
-      for (int w = 0; w < kWalkThreads / 32; w++) {
-        const unsigned x = cnt_s[w];
-        cnt_s[w] = tot;
-        tot += x;
-      }
-      base_s = tot ? atomicAdd(out_count, tot) : 0u;
-    }
-    __syncthreads();
-    if (defer) {
-      const unsigned slot = base_s + cnt_s[wid] + __popc(bal & ((1u << lane) - 1));
-      if (slot < out_cap) {
-        float4* dst = reinterpret_cast<float4*>(oq + slot);
-        __stcs(dst, w0);
-        __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
-                                    __int_as_float(s.idx), __int_as_float(s.cx)));
-        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
-                                    __int_as_float(__double2loint(s.t)),
-                                    __int_as_float(__double2hiint(s.t))));
-      } else {  // queue full: finish here
-        __stcs(out + __float_as_uint(w0.w),
-               T(finish_windows(c, double(w0.x), double(w0.y), a, s)));
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// CTAs per SM for a kernel at 256 threads (one full wave, no partial tail).
-template <class K>
-static int resident_ctas(K kernel) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-  return std::max(per_sm, 1);
-}
-
-template <class T, class I, bool HIT, bool RES>
-static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t, T* out,
-                          int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
-  static const int per_sm = resident_ctas(k_cast<T, I, HIT, RES>);
-  const size_t b = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * per_sm));
-  k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
-}
-
-#ifndef RL_DEFER_MIN_LOG2
-#define RL_DEFER_MIN_LOG2 22
-#endif
-constexpr size_t kDeferMinQueries = size_t(1) << RL_DEFER_MIN_LOG2;
-
-// Dispatch of the batched cast kernels for the device-pointer entry points.
-template <class T>
-static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out,
-                       int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
-  const CddtView v = c->view();
-  const bool small = n < (size_t(1) << 31);
-  if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
-    // stream-ordered scratch: concurrent batches on other streams (e.g. the
-    // pipelined host path) each get their own queue; the pool keeps the
-    // memory reserved, so steady-state allocation is free
-    static const bool pool_ready = [] {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      return true;
-    }();
-    (void)pool_ready;
-    // workspace: counters | n walk records (windows up from 0, near field down
-    // from n-1) | continuation queues A and B (the window passes alternate)
-    // (RL_CDDT_CONT_CAP overrides the queue capacity: a test hook for the
-    // queue-full path)
-    static const size_t cap_env = [] {
-      const char* e = std::getenv("RL_CDDT_CONT_CAP");
-      return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(0);
-    }();
-#ifdef RL_WIN_CAPS_CODE  // A/B builds: decimal digits, e.g. 1124 -> {1, 1, 2, 4}
-    constexpr int kPasses = RL_WIN_CAPS_CODE >= 1000 ? 4 : RL_WIN_CAPS_CODE >= 100 ? 3
-                                                     : RL_WIN_CAPS_CODE >= 10 ? 2 : 1;
-    int kCaps[kPasses];
-    for (int p = kPasses - 1, v = RL_WIN_CAPS_CODE; p >= 0; p--, v /= 10) kCaps[p] = v % 10;
-#else
-    constexpr int kCaps[] = {RL_WIN_CAPS};
-    constexpr int kPasses = sizeof(kCaps) / sizeof(kCaps[0]);  // capped passes; one more runs out
-#endif
-    const size_t cap_a = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_A_DIV, size_t(1) << 16);
-    const size_t cap_b = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_B_DIV, size_t(1) << 16);
-    uint8_t* ws = nullptr;
-    RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws),
-                          256 + sizeof(WalkRecord) * n + sizeof(ContRecord) * (cap_a + cap_b),
-                          st));
-    unsigned* qn = reinterpret_cast<unsigned*>(ws);  // windows, near, one per capped pass
-    WalkRecord* q = reinterpret_cast<WalkRecord*>(ws + 256);
-    ContRecord* qa = reinterpret_cast<ContRecord*>(q + n);
-    ContRecord* qb = qa + cap_a;
-    static const int p1 = [] {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cast_defer_p1<T>, kP1Threads, 0);
-      return std::max(per_sm, 1);
-    }();
-    auto walk_ctas = [](auto kernel) {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWalkThreads, 0);
-      return std::max(per_sm, 1);
-    };
-    static const int pw0 = walk_ctas(k_walk_pass<T, false, false>);
-    static const int pwc = walk_ctas(k_walk_pass<T, true, false>);
-    static const int pwl = walk_ctas(k_walk_pass<T, true, true>);
-    static const int pn = walk_ctas(k_cast_near<T>);
-    RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
-    const size_t b1 = std::max<size_t>(
-        1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
-    k_cast_defer_p1<T><<<int(b1), kP1Threads, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_cast_near<T><<<sm_count() * pn, kWalkThreads, 0, st>>>(v, q, qn, uint32_t(n), qa, qn + 2,
-                                                             uint32_t(cap_a), out);
-    k_walk_pass<T, false, false><<<sm_count() * pw0, kWalkThreads, 0, st>>>(
-        v, q, qn, uint32_t(n), kCaps[0], qa, qn + 2, uint32_t(cap_a), out);
-    for (int p = 1; p < kPasses; p++) {  // queue p-1 -> queue p (A, B, A, ...)
-      const bool from_a = (p & 1) != 0;
-      k_walk_pass<T, true, false><<<sm_count() * pwc, kWalkThreads, 0, st>>>(
-          v, from_a ? qa : qb, qn + 1 + p, uint32_t(from_a ? cap_a : cap_b), kCaps[p],
-          from_a ? qb : qa, qn + 2 + p, uint32_t(from_a ? cap_b : cap_a), out);
-    }
-    const bool last_a = (kPasses & 1) != 0;
-    k_walk_pass<T, true, true><<<sm_count() * pwl, kWalkThreads, 0, st>>>(
-        v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
-        nullptr, 0, out);
-#ifdef RL_DEBUG_COUNTS
-    {
-      unsigned h[2 + kPasses];
-      cudaMemcpyAsync(h, qn, sizeof h, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      fprintf(stderr, "counts n=%zu windows=%u near=%u", n, h[0], h[1]);
-      for (int p = 0; p < kPasses; p++) fprintf(stderr, " after pass %d: %u", p, h[2 + p]);
-      fprintf(stderr, "\n");
-    }
-#endif
-    RL_CK(cudaFreeAsync(ws, st));
-    return RL_OK;
-  }
-  if (rr || ri) {
-    launch_k_cast<T, size_t, true, true>(v, x, y, t, out, hit, rr, ri, n, st);
-  } else if (hit) {
-    if (small)
-      launch_k_cast<T, uint32_t, true, false>(v, x, y, t, out, hit, rr, ri, n, st);
-    else
-      launch_k_cast<T, size_t, true, false>(v, x, y, t, out, hit, rr, ri, n, st);
-  } else {
-    if (small)
-      launch_k_cast<T, uint32_t, false, false>(v, x, y, t, out, hit, rr, ri, n, st);
-    else
-      launch_k_cast<T, size_t, false, false>(v, x, y, t, out, hit, rr, ri, n, st);
-  }
-  return RL_OK;
-}
-
-__global__ void k_directional(CddtView c, const double* __restrict__ x,
-                              const double* __restrict__ y, const int32_t* __restrict__ a,
-                              double* __restrict__ out, size_t n) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x) {
-    CastOut o;
-    out[i] = directional_cast(c, x[i], y[i], a[i], o);
-  }
-}
-
-__global__ void k_single(CddtView c, double x, double y, double theta, int pair,
-                         double* __restrict__ out) {
-  const double th = normalize_angle_2pi(theta);
-  const int a = direction_index(th, c.K);
-  CastOut o;
-  out[0] = directional_cast(c, x, y, a, o);
-  if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
-}
-
-static int dir_blocks(size_t n) {
-  size_t b = (n + 255) / 256;
-  return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * 8)));
-}
-
-// ---------------------------------------------------------------------------
 // K4: prune marking. One state per (free cell centre, direction); the
 // resolving index and its near-side neighbour are marked (cddt.cpp:289-299).
 __global__ void __launch_bounds__(256) k_prune_mark(CddtView c, uint8_t* __restrict__ marks) {
@@ -1039,114 +585,6 @@ int rl_cddt_sync(rl_cddt* c) {
   if (!c) return RL_EINVAL;
   DeviceGuard guard(c->dev);
   RL_CK(cudaStreamSynchronize(c->stream));
-  return RL_OK;
-}
-
-static int single(rl_cddt* c, double x, double y, double theta, int pair, double* o0,
-                  double* o1) {
-  std::lock_guard<std::mutex> lock(c->mu);
-  DeviceGuard guard(c->dev);
-  if (!c->d_scalar.p) RL_TRY(c->d_scalar.alloc(2));
-  k_single<<<1, 1, 0, c->stream>>>(c->view(), x, y, theta, pair, c->d_scalar.p);
-  RL_CK(cudaGetLastError());
-  double r[2];
-  RL_CK(cudaMemcpyAsync(r, c->d_scalar.p, sizeof(double) * (pair ? 2 : 1), cudaMemcpyDeviceToHost,
-                        c->stream));
-  RL_CK(cudaStreamSynchronize(c->stream));
-  *o0 = r[0];
-  if (pair) *o1 = r[1];
-  return RL_OK;
-}
-
-int rl_cddt_cast(rl_cddt* c, double x, double y, double theta, double* out) {
-  if (!c || !out) return RL_EINVAL;
-  return single(c, x, y, theta, 0, out, nullptr);
-}
-
-int rl_cddt_cast_pair(rl_cddt* c, double x, double y, double theta, double* f, double* b) {
-  if (!c || !f || !b) return RL_EINVAL;
-  return single(c, x, y, theta, 1, f, b);
-}
-
-int rl_cddt_cast_batch(rl_cddt* c, const float* x, const float* y, const float* theta, float* out,
-                       int32_t* hit, size_t n, void* stream) {
-  if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
-  if (n == 0) return RL_OK;
-  DeviceGuard guard(c->dev);
-  RL_TRY(launch_cast<float>(c, x, y, theta, out, hit, nullptr, nullptr, n, pick_stream(c, stream)));
-  return finish(c, stream);
-}
-
-int rl_cddt_cast_batch_f64(rl_cddt* c, const double* x, const double* y, const double* theta,
-                           double* out, int32_t* hit, int64_t* res_row, int32_t* res_idx,
-                           size_t n, void* stream) {
-  if (!c || (n && (!x || !y || !theta))) return RL_EINVAL;
-  if (n == 0) return RL_OK;
-  DeviceGuard guard(c->dev);
-  RL_TRY(launch_cast<double>(c, x, y, theta, out, hit, res_row, res_idx, n,
-                             pick_stream(c, stream)));
-  return finish(c, stream);
-}
-
-int rl_cddt_directional_batch(rl_cddt* c, const double* x, const double* y, const int32_t* a,
-                              double* out, size_t n, void* stream) {
-  if (!c || (n && (!x || !y || !a || !out))) return RL_EINVAL;
-  if (n == 0) return RL_OK;
-  DeviceGuard guard(c->dev);
-  k_directional<<<dir_blocks(n), 256, 0, pick_stream(c, stream)>>>(c->view(), x, y, a, out, n);
-  return finish(c, stream);
-}
-
-// Host-buffer batches: chunked H2D -> kernel -> D2H over NSTREAM streams so
-// both copy directions overlap the kernel.
-int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const float* theta,
-                            float* out, size_t n) {
-  if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
-  if (n == 0) return RL_OK;
-  DeviceGuard guard(c->dev);
-  constexpr int NSTREAM = 3;
-  const size_t chunk = std::min<size_t>(n, size_t(1) << 23);  // 8M queries = 128 MB per chunk
-  struct Lane {
-    cudaStream_t s = nullptr;
-    DevBuf<float> buf;  // x | y | theta | out
-  };
-  static thread_local std::vector<Lane> lanes;  // reused across calls on this thread
-  static thread_local size_t lane_chunk = 0;
-  static thread_local int lane_dev = -1;
-  if (lanes.empty() || lane_chunk < chunk || lane_dev != c->dev) {
-    for (auto& l : lanes)
-      if (l.s) cudaStreamDestroy(l.s);
-    lanes.clear();
-    lanes.resize(NSTREAM);
-    for (auto& l : lanes) {
-      RL_CK(cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking));
-      RL_TRY(l.buf.alloc(4 * chunk));
-    }
-    lane_chunk = chunk;
-    lane_dev = c->dev;
-  }
-  cudaEvent_t ready;
-  RL_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
-  const size_t stride = lane_chunk;
-  size_t k = 0;
-  for (size_t off = 0; off < n; off += chunk, k++) {
-    Lane& l = lanes[k % NSTREAM];
-    const size_t m = std::min(chunk, n - off);
-    float* dx = l.buf.p;
-    float* dy = dx + stride;
-    float* dt = dy + stride;
-    float* dout = dt + stride;
-    RL_CK(cudaStreamWaitEvent(l.s, ready, 0));
-    RL_CK(cudaMemcpyAsync(dx, x + off, m * 4, cudaMemcpyHostToDevice, l.s));
-    RL_CK(cudaMemcpyAsync(dy, y + off, m * 4, cudaMemcpyHostToDevice, l.s));
-    RL_CK(cudaMemcpyAsync(dt, theta + off, m * 4, cudaMemcpyHostToDevice, l.s));
-    RL_TRY(launch_cast<float>(c, dx, dy, dt, dout, nullptr, nullptr, nullptr, m, l.s));
-    RL_CK(cudaGetLastError());
-    RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
-  }
-  for (auto& l : lanes) RL_CK(cudaStreamSynchronize(l.s));
-  cudaEventDestroy(ready);
   return RL_OK;
 }
 
