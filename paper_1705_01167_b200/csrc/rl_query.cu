@@ -336,7 +336,10 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
                        int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
-  constexpr size_t kDeferMaxQueries = size_t(1) << 28;  // bounds the record workspace (~12 GB)
+#ifndef RL_DEFER_MAX_LOG2
+#define RL_DEFER_MAX_LOG2 28
+#endif
+  constexpr size_t kDeferMaxQueries = size_t(1) << RL_DEFER_MAX_LOG2;  // bounds the workspace (~12 GB)
   if (!rr && !ri && !hit && n > kDeferMaxQueries) {
     for (size_t off = 0; off < n; off += kDeferMaxQueries) {
       const size_t m = std::min(kDeferMaxQueries, n - off);
