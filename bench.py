@@ -43,6 +43,15 @@ WORKLOAD = dict(
     "(no flush needed)")
 
 
+def workload_config(n: int) -> dict:
+    """WORKLOAD with the query count actually used (--queries)."""
+    if n == WORKLOAD["queries_per_gpu_per_step"]:
+        return dict(WORKLOAD)
+    return dict(WORKLOAD, queries_per_gpu_per_step=n,
+                workload=WORKLOAD["workload"].replace("100M", f"{n / 1e6:g}M"),
+                l2=f"inputs {12 * n / 1e9:.2f} GB/step")
+
+
 def env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -170,11 +179,14 @@ def reference_cpu(g, qx, qy, qt, sample: int, snapshot: bytes | None, threads: i
     return ref, r["out64"], dt, setup, how
 
 
-def pf_update_timing(iterations: int, device: int):
+def pf_update_timing(iterations: int, device: int, group=None):
     """BASELINE config 4: full particle-filter update (motion, fused CDDT sensor
     model with the 501x501 table, normalisation, estimate, low-variance
     resampling) for 40,000 particles x 61 beams on the 2000x2000 maze,
-    theta_disc 120, max_range 500, along a seeded 1 px/step trajectory."""
+    theta_disc 120, max_range 500, along a seeded 1 px/step trajectory.
+    With a process group the particles are sharded over its ranks (one GPU
+    each; every rank calls this) and the step runs with the two NCCL
+    exchanges; per-step times are the max over ranks."""
     import numpy as np
     import torch
 
@@ -189,7 +201,7 @@ def pf_update_timing(iterations: int, device: int):
     table = torch.from_numpy(rl.beam_table(beam, 501, 1.0)).cuda(device)
     cfg = mcl.MclConfig(particle_count=40_000, beam=beam, seed=5,
                         motion=mcl.MotionNoise(1.0, 0.0, 0.0, 0.02))  # sigma_xy 1 px, sigma_th 0.02
-    f = mcl.Mcl(method, cfg, table=table)
+    f = mcl.Mcl(method, cfg, table=table, group=group)
     f.init_gaussian(x, y, t, 10.0, 0.1)
     scans = [torch.from_numpy(synth.scan(g, *pose[k + 1], 61, 4.71238898038469, 500.0, 8.0, 0.05,
                                          seed=1000 + k)).cuda(device) for k in range(iterations)]
@@ -206,8 +218,18 @@ def pf_update_timing(iterations: int, device: int):
         times.append(e0.elapsed_time(e1))
         errs.append(float(np.hypot(r.estimate.x - pose[k + 1][0], r.estimate.y - pose[k + 1][1])))
     times = np.array(times)
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        tt = torch.tensor(times, dtype=torch.float64,
+                          device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=group)
+        times = tt.cpu().numpy()
     return {"workload": "BASELINE config 4: 40,000 particles x 61 beams, 2000x2000 maze, "
-                        "theta_disc=120, 501x501 table, 1 GPU",
+                        f"theta_disc=120, 501x501 table, {world} GPU"
+                        + (f"s (particles sharded, {40_000 // world} per GPU; max over ranks)"
+                           if world > 1 else ""),
             "iterations": iterations, "ms_per_update_p50": float(np.median(times)),
             "ms_per_update_mean": float(times.mean()), "ms_per_update_p99":
             float(np.percentile(times, 99)), "casts_per_update": 40_000 * 61,
@@ -371,10 +393,15 @@ def run_ours(args, rank, world, local_rank):
     value = world * n * args.steps / t_dev
     e2e_value = world * n * args.e2e_steps / t_e2e
     line = None
+    sharded_pf = None
+    if world > 1 and args.pf_iterations > 0:  # every rank: the sharded filter
+        sharded_pf = pf_update_timing(args.pf_iterations, local_rank, group=dist.group.WORLD)
     if rank == 0:
         # GPU extras first: the host-heavy reference sample below leaves CPU
         # worker threads behind that skew host-bound timings
         extras = {}
+        if sharded_pf is not None:
+            extras["pf_update_sharded"] = sharded_pf
         if args.pf_iterations > 0:
             extras["pf_update"] = pf_update_timing(args.pf_iterations, local_rank)
         if not args.no_extra:
@@ -408,7 +435,7 @@ def run_ours(args, rank, world, local_rank):
             "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE config-3 map and query stream)",
-            "config": dict(WORKLOAD, parallelism=f"query-sharded x{world}, structure replicated",
+            "config": dict(workload_config(n), parallelism=f"query-sharded x{world}, structure replicated",
                            zero_points=int(info.zero_points), rows=int(info.rows),
                            device_bytes=int(info.device_bytes),
                            build_plus_prune_s=round(info.init_seconds, 3)),
@@ -458,7 +485,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded BASELINE config-3 map and query stream)",
-        "config": dict(WORKLOAD, parallelism="host threads"),
+        "config": dict(workload_config(args.queries), parallelism="host threads"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{n} queries per step (bounded sample of the 100M-query step) "
                                    f"on the reference's own Cddt (unpruned; its single-threaded "

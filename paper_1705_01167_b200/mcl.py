@@ -231,11 +231,13 @@ def sharded_step(m: "Mcl", stages, dx, dy, dth, it) -> bool:
     m._est = _estimate_from_moments(mom, n, degenerate)
     # exchange 2: resampling gather; every rank resamples its own output slots
     mine = torch.stack([m.x, m.y, m.theta, m.weight])
-    full = torch.empty((m.world, 4, m.n_local), dtype=torch.float64, device=m.x.device)
-    if full.device.type == "cuda":
-        dist.all_gather_into_tensor(full, mine, group=m.group)
+    # rank-concatenated layout (world*4, n_local): accepted by NCCL and gloo
+    flat = torch.empty((m.world * 4, m.n_local), dtype=torch.float64, device=m.x.device)
+    if flat.device.type == "cuda":
+        dist.all_gather_into_tensor(flat, mine, group=m.group)
     else:
-        dist.all_gather(list(full.unbind(0)), mine, group=m.group)
+        dist.all_gather(list(flat.view(m.world, 4, m.n_local).unbind(0)), mine, group=m.group)
+    full = flat.view(m.world, 4, m.n_local)
     allp = full.permute(1, 0, 2).reshape(4, n).contiguous()
     stages.resample(allp, it)
     return degenerate
