@@ -46,6 +46,22 @@ int sm_count() {
   return n;
 }
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; with an unbounded release threshold freed blocks stay reserved, so
+// steady-state allocations cost nothing and never synchronise.
+void retain_pool() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_dev = dev;
+}
+
 int finish(const rl_cddt* c, void* s) {
   RL_CK(cudaGetLastError());
   if (!s) RL_CK(cudaStreamSynchronize(c->stream));

@@ -156,4 +156,5 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
+void retain_pool();                     // the current device's default pool keeps freed memory
 }  // namespace rl

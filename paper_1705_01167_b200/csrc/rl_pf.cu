@@ -417,12 +417,14 @@ int rl_motion_update(double* x, double* y, double* theta, size_t n, uint64_t ind
 int rl_pf_max(const double* logw, size_t n, double* out, void* stream) {
   if (!logw || !out || n == 0) return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool();
   size_t bytes = 0;
   cub::DeviceReduce::Max(nullptr, bytes, logw, out, int(n), s);
-  DevBuf<uint8_t> tmp;
-  RL_TRY(tmp.alloc(bytes));
-  RL_CK(cub::DeviceReduce::Max(tmp.p, bytes, logw, out, int(n), s));
-  RL_CK(cudaStreamSynchronize(s));  // tmp is freed on return
+  void* tmp = nullptr;  // stream-ordered scratch: no synchronisation needed
+  RL_CK(cudaMallocAsync(&tmp, bytes, s));
+  RL_CK(cub::DeviceReduce::Max(tmp, bytes, logw, out, int(n), s));
+  RL_CK(cudaFreeAsync(tmp, s));
+  if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
 
@@ -430,19 +432,21 @@ int rl_pf_weights(const double* logw, const double* gmax, const double* x, const
                   const double* theta, size_t n, double* w, double* moments, void* stream) {
   if (!logw || !gmax || !x || !y || !theta || !w || !moments) return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool();
   if (n == 0) {
     RL_CK(cudaMemsetAsync(moments, 0, 10 * sizeof(double), s));
     RL_CK(cudaStreamSynchronize(s));
     return RL_OK;
   }
   const int nb = moment_blocks(n);
-  DevBuf<double> partial;
-  RL_TRY(partial.alloc(size_t(nb) * 10 + 1));
-  unsigned* ticket = reinterpret_cast<unsigned*>(partial.p + size_t(nb) * 10);
+  double* partial = nullptr;  // stream-ordered scratch: partials | ticket
+  RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&partial), 8 * (size_t(nb) * 10 + 1), s));
+  unsigned* ticket = reinterpret_cast<unsigned*>(partial + size_t(nb) * 10);
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
-  k_weights<<<nb, kPfThreads, 0, s>>>(logw, gmax, x, y, theta, n, w, partial.p, ticket, moments);
+  k_weights<<<nb, kPfThreads, 0, s>>>(logw, gmax, x, y, theta, n, w, partial, ticket, moments);
   RL_CK(cudaGetLastError());
-  RL_CK(cudaStreamSynchronize(s));  // partial is freed on return
+  RL_CK(cudaFreeAsync(partial, s));
+  if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
 
@@ -464,17 +468,19 @@ int rl_resample_low_variance(const double* x, const double* y, const double* the
   if (!x || !y || !theta || !w || !ox || !oy || !otheta || !ow || out_begin + out_count > n)
     return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool();
   const size_t T = scan_tiles(n);
-  DevBuf<double> tmp;  // local[n] | tile_total[T] | tile_excl[T] | ticket
-  RL_TRY(tmp.alloc(n + 2 * T + 1));
-  double *local = tmp.p, *tile_total = local + n, *tile_excl = tile_total + T;
+  double* local = nullptr;  // stream-ordered scratch: local[n] | tile_total[T] | tile_excl[T] | ticket
+  RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&local), 8 * (n + 2 * T + 1), s));
+  double *tile_total = local + n, *tile_excl = tile_total + T;
   unsigned* ticket = reinterpret_cast<unsigned*>(tile_excl + T);
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   k_tile_scan<<<int(T), kPfThreads, 0, s>>>(w, n, local, tile_total, tile_excl, ticket);
   k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, x, y, theta, n, out_begin, out_count,
                                           ox, oy, otheta, ow, seed, iteration);
   RL_CK(cudaGetLastError());
-  RL_CK(cudaStreamSynchronize(s));  // tmp is freed on return
+  RL_CK(cudaFreeAsync(local, s));
+  if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
 

@@ -352,17 +352,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     // stream-ordered scratch: concurrent batches on other streams (e.g. the
     // pipelined host path) each get their own queue; the pool keeps the
     // memory reserved, so steady-state allocation is free
-    static const bool pool_ready = [] {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      return true;
-    }();
-    (void)pool_ready;
+    retain_pool();
     // workspace: counters | n walk records (windows up from 0, near field down
     // from n-1) | continuation queues A and B (the window passes alternate)
     // (RL_CDDT_CONT_CAP overrides the queue capacity: a test hook for the

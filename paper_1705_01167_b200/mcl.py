@@ -226,8 +226,8 @@ def sharded_step(m: "Mcl", stages, dx, dy, dth, it) -> bool:
     stages.weights()  # exp(logw - max) and pose moments
     dist.all_reduce(m.moments, op=dist.ReduceOp.SUM, group=m.group)  # exchange 1b: weight sum
     stages.normalize()
-    mom = m.moments.cpu().numpy()
-    degenerate = bool(m.flag.item())
+    both = torch.cat([m.moments, m.flag.to(torch.float64)]).cpu().numpy()  # one read-back
+    mom, degenerate = both[:10], bool(both[10])
     m._est = _estimate_from_moments(mom, n, degenerate)
     # exchange 2: resampling gather; every rank resamples its own output slots
     mine = torch.stack([m.x, m.y, m.theta, m.weight])
