@@ -673,3 +673,30 @@ def test_f64_batch_optional_outputs(rl, synth):
         torch.cuda.synchronize()
         for k, v in part.items():
             assert torch.equal(v, full[k]), (mask, k)
+
+
+@pytest.mark.parametrize("seed", [101, 202, 303])
+def test_split_path_random_structures(rl, oracle_mod, synth, seed):
+    """Randomised split-path parity: odd map sizes (not multiples of 32),
+    random occupancy, theta_disc and max_range, CDDT and PCDDT, 4M+ queries
+    from anywhere around the map, bit-exact against the restatement."""
+    import torch
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(37, 300)), int(rng.integers(5, 260))
+    g = (rng.random((h, w)) < rng.uniform(0.02, 0.3)).astype(np.uint8)
+    K = int(rng.integers(2, 160)) * 2
+    mr = float(rng.choice([0.0, rng.uniform(0.5, 4.0), rng.uniform(5.0, 400.0)]))
+    prune = bool(seed % 2)
+    n = (1 << 22) + int(rng.integers(0, 100_000))
+    qx = rng.uniform(-2, w + 2, n).astype(np.float32)
+    qy = rng.uniform(-2, h + 2, n).astype(np.float32)
+    qt = rng.uniform(-7, 13, n).astype(np.float32)
+    gpu = make_gpu(rl, g, K, mr, prune=prune)
+    got = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
+    torch.cuda.synchronize()
+    orc = oracle_mod.OracleCddt(g, K, mr)
+    if prune:
+        orc.prune()
+    want = orc.cast_batch(qx, qy, qt, want_f64=False, want_hit=False, want_res=False)["out32"]
+    bad = np.flatnonzero(host(got).view(np.uint32) != want.view(np.uint32))
+    assert bad.size == 0, (w, h, K, mr, prune, bad[:10])
