@@ -1,3 +1,6 @@
+# Round-end measurement on a B200 box (run through gpurun): the GPU test suite,
+# smoke(), the bench line and the reference arm, the ncu launch list and one
+# ncu --set full capture of a config-3 step. Outputs land in gpurun_out/.
 set -x
 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
