@@ -382,6 +382,10 @@ struct CastOut {
   int32_t res_idx;  // index within the row, -1 when no zero point resolved
 };
 
+struct __align__(32) RowRecord {
+  float4 a, b;
+};
+
 // Per-query geometry shared by the whole and the split forms.
 struct QueryRow {
   bool forward;
@@ -402,9 +406,10 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   q.g = sp.row_base + (uint32_t)row;
   // requested together with the origin cell's bits: the two are independent
-  const float4* rec = reinterpret_cast<const float4*>(c.hints + size_t(q.g) * kHintFloats);
-  q.hint = __ldg(rec);
-  q.hint2 = __ldg(rec + 1);
+  // one 32-byte load (LDG.256) rather than two 16-byte ones: one L1 wavefront per lane
+  const RowRecord rec = reinterpret_cast<const RowRecord*>(c.hints)[q.g];
+  q.hint = rec.a;
+  q.hint2 = rec.b;
   q.lo = __float_as_uint(q.hint.x);
   q.hi = q.lo + __float_as_uint(q.hint.y);
   return q;
