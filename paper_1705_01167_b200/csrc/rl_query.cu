@@ -48,11 +48,25 @@ __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict
 // The window passes (k_walk_pass) resume exactly there, every lane walking;
 // near-field queries are redone in full by k_cast_near. Records are streamed
 // evict-first past L2.
-struct __align__(16) WalkRecord {
+struct __align__(32) WalkRecord {
   float x, y, t;
   uint32_t i, lo, n;
   int32_t idx, pad;
 };
+
+// A 32-byte record moved by one 256-bit evict-first access (LDG/STG.E.EF.256):
+// one L1 wavefront per lane instead of two.
+__device__ __forceinline__ void ld256_cs(const void* p, float4& a, float4& b) {
+  asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256_cs(void* p, const float4& a, const float4& b) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x),
+               "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
 
 #ifndef RL_P1_CTAS
 #define RL_P1_CTAS 6  // resident CTAs per SM the register budget of phase 1 targets
@@ -133,9 +147,7 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
       const size_t slot = win ? base_s[0] + cnt_s[0][wid] + __popc(bw & below)
                               : n - 1 - (base_s[1] + cnt_s[1][wid] + __popc(bn & below));
       const float4* src = reinterpret_cast<const float4*>(&rec);
-      float4* dst = reinterpret_cast<float4*>(q + slot);
-      __stcs(dst, src[0]);
-      __stcs(dst + 1, src[1]);
+      st256_cs(q + slot, src[0], src[1]);
     }
     __syncthreads();
   }
@@ -203,8 +215,8 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
                      __float_as_int(w1.w), __float_as_int(w2.x),
                      __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z)), 0.f};
       } else {
-        const float4* src = reinterpret_cast<const float4*>(static_cast<const WalkRecord*>(in) + k);
-        const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1);
+        float4 w0, w1;
+        ld256_cs(static_cast<const WalkRecord*>(in) + k, w0, w1);
         fx = w0.x;
         fy = w0.y;
         ft = w0.z;
