@@ -568,6 +568,10 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
   }
   cudaEvent_t ready;
   RL_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  struct EventGuard {  // released on every return path
+    cudaEvent_t e;
+    ~EventGuard() { cudaEventDestroy(e); }
+  } ready_guard{ready};
   RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
   const size_t stride = lane_chunk;
   size_t k = 0;
@@ -587,7 +591,6 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
     RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
   }
   for (auto& l : lanes) RL_CK(cudaStreamSynchronize(l.s));
-  cudaEventDestroy(ready);
   return RL_OK;
 }
 
