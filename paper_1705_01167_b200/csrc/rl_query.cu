@@ -574,10 +574,27 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
   } ready_guard{ready};
   RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
   const size_t stride = lane_chunk;
-  size_t k = 0;
-  for (size_t off = 0; off < n; off += chunk, k++) {
-    Lane& l = lanes[k % NSTREAM];
-    const size_t m = std::min(chunk, n - off);
+  // Chunk plan. The link is the bottleneck; once the last upload is done it
+  // idles for the last chunk's cast and download, so the final `chunk`
+  // queries go as a ramp of halving chunks (1/2, 1/4, 1/8, 1/8).
+  static const bool ramp = [] {
+    const char* e = std::getenv("RL_HOST_RAMP");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  std::vector<size_t> plan;
+  const size_t tail = ramp ? std::min(n, chunk) : 0;
+  for (size_t b = n - tail; b > 0;) {
+    plan.push_back(std::min(chunk, b));
+    b -= plan.back();
+  }
+  for (size_t rem = tail, part = 0; rem > 0; part++) {
+    const size_t m = part < 3 ? std::max<size_t>(1, tail >> (part + 1)) : rem;
+    plan.push_back(std::min(m, rem));
+    rem -= plan.back();
+  }
+  size_t k = 0, off = 0;
+  for (const size_t m : plan) {
+    Lane& l = lanes[k++ % NSTREAM];
     float* dx = l.buf.p;
     float* dy = dx + stride;
     float* dt = dy + stride;
@@ -589,6 +606,7 @@ int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const fl
     RL_TRY(launch_cast<float>(c, dx, dy, dt, dout, nullptr, nullptr, nullptr, m, l.s));
     RL_CK(cudaGetLastError());
     RL_CK(cudaMemcpyAsync(out + off, dout, m * 4, cudaMemcpyDeviceToHost, l.s));
+    off += m;
   }
   for (auto& l : lanes) RL_CK(cudaStreamSynchronize(l.s));
   return RL_OK;

@@ -1,5 +1,6 @@
 """Config-3 end-to-end timing through the host-pointer C ABI (pinned host
 buffers, H2D + casts + D2H): python scripts/e2e_timing.py"""
+import hashlib
 import os
 import sys
 from pathlib import Path
@@ -24,4 +25,5 @@ for _ in range(3):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
-print({"lib": os.environ.get("RL_CDDT_LIB", "default"), "ms": ms, "gcasts_per_s": n / ms / 1e6})
+print({"lib": os.environ.get("RL_CDDT_LIB", "default"), "ramp": os.environ.get("RL_HOST_RAMP", "default"),
+       "ms": ms, "gcasts_per_s": n / ms / 1e6, "sha": hashlib.sha256(ho.tobytes()).hexdigest()[:16]})
