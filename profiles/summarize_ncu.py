@@ -19,6 +19,10 @@ KEYS = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__inst_executed.sum",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "smsp__sass_average_branch_targets_threads_uniform.pct",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
 
 
