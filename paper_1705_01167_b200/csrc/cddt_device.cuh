@@ -46,6 +46,8 @@ struct CddtView {
   const float* __restrict__ hints;        // rows x kHintFloats: row records (CSR range + probes)
   const SliceParam* __restrict__ slices;  // S
   const double4* __restrict__ dirs;       // K (cos, sin, 1/cos, 1/sin), axis-snapped (cddt.cpp:30-42)
+  const double4* __restrict__ pdirs;      // K (slice cos, slice sin, direction cos, direction sin)
+  const uint32_t* __restrict__ rbase;     // S: slice row bases (4 B each: a few lines in all)
   int w, h, K, S;
   double max_range;
 };
@@ -415,6 +417,49 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   return q;
 }
 
+// SliceProjection::make's offset and bin count (cddt.cpp:44-60), recomputed
+// from the slice's cos/sin with the host's operations (init_geometry), so
+// bit-identical to the table values.
+__device__ __forceinline__ void slice_extent(const CddtView& c, double cs, double sn,
+                                             double* y_offset, int* bin_count) {
+  const double A = 0.0, B = -double(c.w) * sn, C = double(c.h) * cs, D = B + C;
+  const double lo = fmin_std(fmin_std(A, B), fmin_std(C, D));
+  const double hi = fmax_std(fmax_std(A, B), fmax_std(C, D));
+  *y_offset = -lo;
+  *bin_count = int(ceil(hi - lo)) + 1;
+}
+
+// query_row for the batch phase 1: one 32-byte per-direction entry (slice
+// cos/sin and the direction's cos/sin) instead of the slice table plus the
+// direction table, the slice's offset and bin count recomputed, the row
+// record via the compact row-base table. Returns the direction in *dir.
+__device__ __forceinline__ QueryRow query_row_p1(const CddtView& c, double x, double y, int a,
+                                                 double2* dir) {
+  QueryRow q;
+  q.forward = a < c.S;
+  const int s = q.forward ? a : a - c.S;
+  double4 pd;  // one 256-bit load: a single L1 wavefront per lane
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(pd.x), "=d"(pd.y), "=d"(pd.z), "=d"(pd.w)
+      : "l"(c.pdirs + a));
+  *dir = make_double2(pd.z, pd.w);
+  double y_offset;
+  int bin_count;
+  slice_extent(c, pd.x, pd.y, &y_offset, &bin_count);
+  q.xq = x * pd.x + y * pd.y;                            // cddt.hpp:31
+  const double yq = -x * pd.y + y * pd.x + y_offset;     // cddt.hpp:32
+  int row = (int)yq;
+  if (row < 0) row = 0;
+  if (row >= bin_count) row = bin_count - 1;
+  q.g = __ldg(c.rbase + s) + uint32_t(row);
+  const RowRecord rec = reinterpret_cast<const RowRecord*>(c.hints)[q.g];
+  q.hint = rec.a;
+  q.hint2 = rec.b;
+  q.lo = __float_as_uint(q.hint.x);
+  q.hi = q.lo + __float_as_uint(q.hint.y);
+  return q;
+}
+
 // Landing-cell probe (cddt.cpp:239-253): the point at distance d settles the
 // candidate when it lies strictly inside an occupied cell.
 __device__ __forceinline__ bool landing_hit(const CddtView& c, double px, double py,
@@ -512,7 +557,8 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
     *result = c.max_range;
     return true;
   }
-  const QueryRow q = query_row(c, x, y, a);
+  double2 dir;
+  const QueryRow q = query_row_p1(c, x, y, a, &dir);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {
     *result = 0.0;
@@ -529,7 +575,6 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
       partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint, q.hint2);
   const int n = (int)(q.hi - q.lo);
   const int step = q.forward ? 1 : -1;
-  const double4 dir = c.dirs[a];
   for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
        idx += step) {
     const float fv = uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx);

@@ -112,6 +112,19 @@ int init_geometry(rl_cddt* c) {
   c->rows = base;
   RL_TRY(c->d_slices.alloc(c->S));
   RL_TRY(c->d_dirs.alloc(c->K));
+  RL_TRY(c->d_pdirs.alloc(c->K));
+  RL_TRY(c->d_rbase.alloc(c->S));
+  std::vector<double4> pdirs(c->K);
+  for (int a = 0; a < c->K; a++) {
+    const int s = a < c->S ? a : a - c->S;
+    pdirs[a] = make_double4(c->dcos[s], c->dsin[s], c->dcos[a], c->dsin[a]);
+  }
+  std::vector<uint32_t> rbase(c->S);
+  for (int s = 0; s < c->S; s++) rbase[s] = c->slices[s].row_base;
+  RL_CK(cudaMemcpyAsync(c->d_pdirs.p, pdirs.data(), sizeof(double4) * c->K, cudaMemcpyHostToDevice,
+                        c->stream));
+  RL_CK(cudaMemcpyAsync(c->d_rbase.p, rbase.data(), sizeof(uint32_t) * c->S,
+                        cudaMemcpyHostToDevice, c->stream));
   // reciprocals for the walker's boundary divisions (cddt_device.cuh div_rn)
   std::vector<double4> dirs(c->K);
   for (int a = 0; a < c->K; a++)
@@ -557,6 +570,8 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->hints.release();
     c->d_slices.release();
     c->d_dirs.release();
+    c->d_pdirs.release();
+    c->d_rbase.release();
     c->d_scalar.release();
     c->ws.release();
     c->upd_ws.release();
@@ -592,7 +607,7 @@ int rl_cddt_info(const rl_cddt* c, rl_cddt_info_t* o) {
   o->memory_bytes = 4 * c->zero_points + (wh + 7) / 8 + uint64_t(c->S) * 48;  // cddt.hpp:200-203
   o->device_bytes = c->flags.bytes() + c->rowbits.bytes() + c->row_off.bytes() +
                     c->hints.bytes() + 4 * c->zero_points + c->d_slices.bytes() +
-                    c->d_dirs.bytes();
+                    c->d_dirs.bytes() + c->d_pdirs.bytes() + c->d_rbase.bytes();
   o->init_seconds = c->init_seconds;
   return RL_OK;
 }

@@ -115,10 +115,12 @@ struct rl_cddt {
   rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
   int wpr = 0;
   rl::DevBuf<uint32_t> row_off;     // rows+1
-  rl::DevBuf<float> hints;          // rows x kHintFloats: search hints (cddt_device.cuh)
+  rl::DevBuf<float> hints;          // rows x kHintFloats: row records (cddt_device.cuh)
   rl::DevBuf<float> zp;             // capacity >= zero_points
   rl::DevBuf<rl::SliceParam> d_slices;
   rl::DevBuf<double4> d_dirs;   // cos, sin, 1/cos, 1/sin
+  rl::DevBuf<double4> d_pdirs;  // per direction: slice cos, slice sin, cos, sin (batch phase 1)
+  rl::DevBuf<uint32_t> d_rbase;  // S slice row bases (batch phase 1)
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
   std::mutex mu;                    // serialises users of d_scalar / ws / pf_* / the handle stream
@@ -139,6 +141,8 @@ struct rl_cddt {
     v.hints = hints.p;
     v.slices = d_slices.p;
     v.dirs = d_dirs.p;
+    v.pdirs = d_pdirs.p;
+    v.rbase = d_rbase.p;
     v.w = w;
     v.h = h;
     v.K = K;
