@@ -483,18 +483,18 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   o.res_g = 0;
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) return c.max_range;  // cddt.cpp:209
-  const QueryRow q = query_row(c, x, y, a);
+  double2 d2;  // the direction's cos/sin; the walker's full entry is read when one is needed
+  const QueryRow q = query_row_p1(c, x, y, a, &d2);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {  // cddt.cpp:210
     o.hit = cyi * c.w + cxi;
     return 0.0;
   }
-  const double4 dir = c.dirs[a];
   Walker<false> wk;
   bool have_walker = false;
   if (!((w0.y >> (cxi & 31)) & 1u)) {
     // something occupied within one cell: resolve the near field exactly (cddt.cpp:225-232)
-    wk.init_at(x, y, dir, 0.0);
+    wk.init_at(x, y, c.dirs[a], 0.0);
     have_walker = true;
     const double r = wk.scan_to(c, kNearField);
     if (r >= 0.0) {
@@ -515,7 +515,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     const double d = q.forward ? vv - q.xq : q.xq - vv;
     if (d >= c.max_range) break;
     int32_t cell;
-    if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {
+    if (landing_hit(c, x + d * d2.x, y + d * d2.y, &cell)) {
       o.hit = cell;
       o.res_g = q.g;
       o.res_idx = idx;
@@ -523,7 +523,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
     }
     // verification window around the candidate (cddt.cpp:254-261)
     if (!have_walker) {
-      wk.init_at(x, y, dir, d - kVerifyHalf);
+      wk.init_at(x, y, c.dirs[a], d - kVerifyHalf);
       have_walker = true;
     } else {
       wk.seek(d - kVerifyHalf);
