@@ -532,15 +532,21 @@ def test_deferred_path_edge_cases(rl, oracle_mod):
 
 def test_deferred_path_equals_single_kernel_cfg3(rl, synth):
     """Config-3 PCDDT: the split f32 batch equals float() of the single-kernel
-    f64 batch on 8M queries."""
+    f64 batch on 8M queries, and the pipelined host-buffer path (an 8M-query
+    body chunk plus the 4M/2M/1M/1M tail ramp, split and single-kernel chunks
+    mixed) returns the same ranges."""
     import torch
     g = synth.polygon_map()
     gpu = make_gpu(rl, g, 200, 1000.0, prune=True)
-    qx, qy, qt = synth.free_queries(g, 8_000_000, seed=77)
+    n = 8_000_000 + (1 << 23) + 12_345
+    qx, qy, qt = synth.free_queries(g, n, seed=77)
     split = gpu.cast_batch(dev(qx), dev(qy), dev(qt))
-    whole = gpu.cast_batch_f64(*(dev(a.astype(np.float64)) for a in (qx, qy, qt)))
+    m = 8_000_000
+    whole = gpu.cast_batch_f64(*(dev(a[:m].astype(np.float64)) for a in (qx, qy, qt)))
     torch.cuda.synchronize()
-    assert torch.equal(split, whole.float())
+    assert torch.equal(split[:m], whole.float())
+    hosted = gpu.cast_batch(qx, qy, qt)
+    assert np.array_equal(hosted, host(split))
 
 
 def test_concurrent_batches_on_two_streams(rl, synth):
