@@ -233,29 +233,6 @@ struct Walker {
   }
 };
 
-// Number of leading elements e of v[0, n) with pred(e): double(e) <= xq
-// (forward: !(xq < e), std::upper_bound) or double(e) < xq (backward,
-// std::lower_bound), with libstdc++'s halving sequence (cddt.hpp:106-131).
-// The comparisons run in the float domain, exactly: for a float e,
-//   double(e) <= xq  <=>  e <= RD_f32(xq)     and     double(e) < xq  <=>  e < RU_f32(xq)
-// (no float lies strictly between RD_f32(xq) and RU_f32(xq)).
-__device__ __forceinline__ uint32_t partition_point(const float* __restrict__ v, uint32_t n,
-                                                    double xq, bool forward) {
-  const float xlo = __double2float_rd(xq), xhi = __double2float_ru(xq);
-  uint32_t first = 0, len = n;
-  while (len > 0) {
-    const uint32_t half = len >> 1, mid = first + half;
-    const float e = __ldg(v + mid);
-    if (forward ? (e <= xlo) : (e < xhi)) {
-      first = mid + 1;
-      len -= half + 1;
-    } else {
-      len = half;
-    }
-  }
-  return first;
-}
-
 // Row records: one 32-byte sector per row with the CSR range and the zero
 // points the row's binary search probes first, so a query's first three
 // search steps arrive with its row instead of one round trip each:
@@ -290,8 +267,14 @@ __host__ __device__ __forceinline__ bool hint_index(uint32_t n, int level, uint3
   }
 }
 
-// partition_point with its first kHintLevels steps taken from the row's
-// hints: the same index sequence and comparisons, so the same result. It also
+// Number of leading elements e of v[0, n) with double(e) <= xq (forward:
+// !(xq < e), std::upper_bound) or double(e) < xq (backward, std::lower_bound),
+// with libstdc++'s halving sequence (cddt.hpp:106-131). The comparisons run in
+// the float domain, exactly: for a float e,
+//   double(e) <= xq  <=>  e <= RD_f32(xq)     and     double(e) < xq  <=>  e < RU_f32(xq)
+// (no float lies strictly between RD_f32(xq) and RU_f32(xq)). The first
+// kHintLevels steps are taken from the row record: the same index sequence
+// and comparisons, so the same result. It also
 // reports the first candidate's zero point when the search probed it (the
 // forward candidate is the leftmost failing probe, the backward one the
 // rightmost passing probe), which saves that load for short rows.
@@ -429,11 +412,11 @@ __device__ __forceinline__ void slice_extent(const CddtView& c, double cs, doubl
   *bin_count = int(ceil(hi - lo)) + 1;
 }
 
-// query_row for the batch phase 1: one 32-byte per-direction entry (slice
-// cos/sin and the direction's cos/sin) instead of the slice table plus the
-// direction table, the slice's offset and bin count recomputed, the row
-// record via the compact row-base table. Returns the direction in *dir.
-__device__ __forceinline__ QueryRow query_row_p1(const CddtView& c, double x, double y, int a,
+// The query's slice row and its record: one 32-byte per-direction entry
+// (slice cos/sin and the direction's cos/sin) rather than the slice and
+// direction records, the slice's offset and bin count recomputed, the row
+// base from the 4-byte-per-slice table. Returns the direction in *dir.
+__device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, double y, int a,
                                                  double2* dir) {
   QueryRow q;
   q.forward = a < c.S;
@@ -484,7 +467,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) return c.max_range;  // cddt.cpp:209
   double2 d2;  // the direction's cos/sin; the walker's full entry is read when one is needed
-  const QueryRow q = query_row_p1(c, x, y, a, &d2);
+  const QueryRow q = query_row(c, x, y, a, &d2);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {  // cddt.cpp:210
     o.hit = cyi * c.w + cxi;
@@ -558,7 +541,7 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
     return true;
   }
   double2 dir;
-  const QueryRow q = query_row_p1(c, x, y, a, &dir);
+  const QueryRow q = query_row(c, x, y, a, &dir);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {
     *result = 0.0;
