@@ -16,7 +16,9 @@ CUDA events on the launching stream with the queries already resident in HBM
 and the D2H copy of the ranges inside the timed region.
 
 --impl reference times the reference's own CPU implementation (the unmodified
-rangelib compiled into oracle/_ref) on the host cores with all threads.
+rangelib compiled into oracle/_ref) on the host cores with all threads. Both
+arms also time the reference's ray-marching method on a bounded sample of the
+same queries (cpu_baseline.ray_march).
 """
 from __future__ import annotations
 
@@ -177,6 +179,23 @@ def reference_cpu(g, qx, qy, qt, sample: int, snapshot: bytes | None, threads: i
     r = ref.cast_batch(xs, ys, ts, want_res=False, threads=threads)
     dt = time.perf_counter() - t0
     return ref, r["out64"], dt, setup, how
+
+
+def ray_march_cpu(g, qx, qy, qt, sample: int, threads: int) -> dict:
+    """The reference's other CPU path for the same queries: make_method(ray_march)
+    (proj/src/methods.cpp:55-72), timed on a bounded sample with all threads."""
+    import oracle
+    oracle.build(ref=True)
+    t0 = time.perf_counter()
+    rm = oracle.RefRayMarch(g, 1000.0)
+    setup = time.perf_counter() - t0
+    rm.cast_batch(qx[:10000], qy[:10000], qt[:10000], threads=threads)
+    t0 = time.perf_counter()
+    rm.cast_batch(qx[:sample], qy[:sample], qt[:sample], threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{sample} queries of this workload through make_method(ray_march), "
+                      f"construction {setup:.2f} s"}
 
 
 def pf_update_timing(iterations: int, device: int, group=None):
@@ -455,7 +474,9 @@ def run_ours(args, rank, world, local_rank):
                              "kind": "reference",
                              "sample": f"{sample} queries of this workload on {how}; "
                                        f"{cpu_model()}",
-                             "parity_mismatches": mism},
+                             "parity_mismatches": mism,
+                             "ray_march": ray_march_cpu(g, qx.numpy(), qy.numpy(), qt.numpy(),
+                                                        min(n, args.rm_sample), threads)},
             "clocks": clk.summary(),
         }
         line.update(extras)
@@ -490,7 +511,9 @@ def run_reference(args):
                          "sample": f"{n} queries per step (bounded sample of the 100M-query step) "
                                    f"on the reference's own Cddt (unpruned; its single-threaded "
                                    f"prune of this map takes minutes), build {build_s:.1f} s; "
-                                   f"{cpu_model()}"},
+                                   f"{cpu_model()}",
+                         "ray_march": ray_march_cpu(g, xs, ys, ts, min(n, args.rm_sample),
+                                                    threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -506,6 +529,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=16_000_000)
     ap.add_argument("--sector-sample", type=int, default=200_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--rm-sample", type=int, default=1_000_000,
+                    help="queries for the reference's ray-marching CPU timing")
     ap.add_argument("--pf-iterations", type=int, default=1000)
     ap.add_argument("--no-extra", action="store_true", help="skip the config 1/2/5 timings")
     args = ap.parse_args()
