@@ -142,7 +142,8 @@ def make_workload(n_queries: int, rank: int, on_gpu: bool = True):
 
     from paper_1705_01167_b200 import synth
     g = synth.polygon_map(4000, 4000, 0.12, seed=3)
-    qx, qy, qt = (torch.empty(n_queries, dtype=torch.float32).pin_memory() for _ in range(3))
+    pin = torch.cuda.is_available()  # the reference arm also runs on a host without a GPU
+    qx, qy, qt = (torch.empty(n_queries, dtype=torch.float32, pin_memory=pin) for _ in range(3))
     if on_gpu and torch.cuda.is_available():
         gd = torch.from_numpy(g).cuda()
         dq = synth.free_queries_gpu(gd, 4000, 4000, n_queries, seed=7, start=rank * n_queries)
