@@ -579,6 +579,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->off_spare.release();
     c->pf_ctl.release();
     if (c->pf_host) cudaFreeHost(c->pf_host);
+    if (c->host_small) cudaFreeHost(c->host_small);
     if (c->stream) cudaStreamDestroy(c->stream);
   }
   delete c;

@@ -127,6 +127,7 @@ struct rl_cddt {
   rl::DevBuf<uint8_t> pf_ctl;       // fused PF step: {max key, ticket} | moments (zeroed when dirty)
   bool pf_ctl_clean = false;        // the max key is 0 (every completed step leaves it so)
   void* pf_host = nullptr;          // fused PF step: pinned host copy of the moments
+  uint32_t* host_small = nullptr;   // 64 pinned bytes for small read-backs (flags, counts)
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off
@@ -161,4 +162,18 @@ int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
 void retain_pool();                     // the current device's default pool keeps freed memory
+// 16 pinned u32 for small device->host read-backs (a pageable destination
+// would add a staging copy to every synchronous step)
+inline int host_small(rl_cddt* c, uint32_t** out) {
+  if (!c->host_small) {
+    const cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&c->host_small), 64);
+    if (e != cudaSuccess) {
+      c->host_small = nullptr;
+      set_error("cudaMallocHost(64): %s", cudaGetErrorString(e));
+      return RL_ENOMEM;
+    }
+  }
+  *out = c->host_small;
+  return RL_OK;
+}
 }  // namespace rl

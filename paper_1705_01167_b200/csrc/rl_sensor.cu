@@ -338,10 +338,11 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   void* args[] = {&d_logw, &key, &d_w, &nn, &partial, &d_flag};
   RL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sensor_normalize), dim3(nblk),
                                     dim3(256), args, 0, st));
-  int flag = 0;
-  RL_CK(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  uint32_t* hs = nullptr;
+  RL_TRY(host_small(c, &hs));
+  RL_CK(cudaMemcpyAsync(hs, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
-  return flag ? RL_EDEGENERATE : RL_OK;
+  return hs[0] ? RL_EDEGENERATE : RL_OK;
 }
 
 }  // extern "C"

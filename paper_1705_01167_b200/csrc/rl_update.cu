@@ -380,7 +380,8 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
       c->row_off.p, c->zp.p, new_off, c->zp_spare.p, add_cnt, rem_cnt, keys_sorted, vals_sorted,
       unsigned(cap), rows, d_count + 1);
   RL_CK(cudaGetLastError());
-  uint32_t total_miss[2] = {0, 0};
+  uint32_t* total_miss = nullptr;  // pinned: {new zero-point total, missed removals}
+  RL_TRY(host_small(c, &total_miss));
   RL_CK(cudaMemcpyAsync(&total_miss[0], new_off + rows, 4, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaMemcpyAsync(&total_miss[1], d_count + 1, 4, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
