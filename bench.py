@@ -182,6 +182,27 @@ def reference_cpu(g, qx, qy, qt, sample: int, snapshot: bytes | None, threads: i
     return ref, r["out64"], dt, setup, how
 
 
+def gather_ceiling(device: int) -> dict:
+    """Scattered-sector read rates (rl_diag_gather: independent 16-byte reads of
+    random 32-byte sectors, full occupancy) out of buffers the size of the
+    config-3 query working set (L2) and far beyond L2 (HBM), in G sectors/s."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1705_01167_b200._lib import check, lib, torch_stream
+    out = {}
+    for name, nbytes in (("l2_16MB", 16 << 20), ("l2_111MB", 111 << 20), ("hbm_4GB", 4 << 30)):
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+        buf.random_()
+        ms, issued = C.c_double(), C.c_uint64()
+        check(lib().rl_diag_gather(buf.data_ptr(), nbytes, 1 << 30, torch_stream(buf.device),
+                                   C.byref(ms), C.byref(issued)))
+        out[name] = issued.value / ms.value / 1e6
+        del buf
+    return out
+
+
 def ray_march_cpu(g, qx, qy, qt, sample: int, threads: int) -> dict:
     """The reference's other CPU path for the same queries: make_method(ray_march)
     (proj/src/methods.cpp:55-72), timed on a bounded sample with all threads."""
@@ -449,6 +470,11 @@ def run_ours(args, rank, world, local_rank):
         traffic = None
         if tr and tr.get("dram_bytes_per_query"):
             traffic = tr["dram_bytes_per_query"] * n
+        # the scattered-read ceiling beside the cast's algorithmic scattered-sector rate
+        gather = gather_ceiling(local_rank)
+        gather["cast_algorithmic"] = s_bar * n * args.steps / t_dev / 1e9
+        gather["frac_of_l2_111MB"] = gather["cast_algorithmic"] / gather["l2_111MB"]
+        gather["unit"] = "G sectors/s (random 32-byte sectors; cast: S-bar sectors per query)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -470,7 +496,8 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_query": bytes_per_query, "sectors_per_query": s_bar,
                          "sector_sample": ns,
                          "kernel": "batched cast = k_cast_defer_p1 + k_cast_near + 4 x k_walk_pass (window "
-                                   "passes) back to back; timed per step"},
+                                   "passes) back to back; timed per step",
+                         "gather_ceiling": gather},
             "cpu_baseline": {"value": sample / ref_dt, "unit": UNIT, "cores": threads,
                              "kind": "reference",
                              "sample": f"{sample} queries of this workload on {how}; "

@@ -163,6 +163,14 @@ int rl_simulate_scans(rl_cddt *c, const double *x, const double *y, const double
 /* Wait for all work queued on the handle's stream. */
 int rl_cddt_sync(rl_cddt *c);
 
+/* Diagnostic (no reference counterpart): the scattered-read ceiling the cast
+ * kernels are measured against. Issues about `loads` independent 16-byte reads,
+ * each in a random 32-byte sector of the device buffer `buf` (`bytes` long),
+ * eight in flight per thread at full occupancy; returns the elapsed device
+ * time (*ms) and the reads actually issued (*issued). Synchronous. */
+int rl_diag_gather(const void *buf, size_t bytes, size_t loads, void *stream, double *ms,
+                   uint64_t *issued);
+
 /* ---- beam sensor model and particle filter (proj/src/mcl.cpp) ---- */
 
 /* BeamModelParams (proj/include/rangelib/mcl.hpp:32-40). */
