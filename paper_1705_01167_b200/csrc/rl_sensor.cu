@@ -78,11 +78,19 @@ __device__ __forceinline__ double item_loglike(double e, int b, const double* __
 // MOTION: the CTA's particles first take their motion_update step (the fused
 // Mcl::step, mcl.cpp:189-193) and write the moved poses back. gmax_key (may be
 // null) receives the order-preserving atomic max of the log-weights.
+// Resident CTAs per SM: 4 (64 registers, a few bytes of spill) for the large
+// sets, where throughput decides (config 4); 3 (74 registers, no spill) for
+// the small ones, where the slowest cast decides (config 2: -3.5 %).
 #ifndef RL_SENSOR_MINB
-#define RL_SENSOR_MINB 4  // resident CTAs per SM (caps registers at 64)
+#define RL_SENSOR_MINB 4
+#endif
+#ifndef RL_SENSOR_MINB_SMALL
+#define RL_SENSOR_MINB_SMALL 3
 #endif
 template <bool MOTION, int kSensorParticlesPerCta>
-__global__ void __launch_bounds__(256, RL_SENSOR_MINB) k_sensor_logw(
+__global__ void __launch_bounds__(256, kSensorParticlesPerCta < 16 ? RL_SENSOR_MINB_SMALL
+                                                                   : RL_SENSOR_MINB)
+    k_sensor_logw(
     CddtView c, double* __restrict__ px, double* __restrict__ py, double* __restrict__ pt,
     size_t n, const double* __restrict__ scan, int nb, double fov, BeamParams bp,
     const float* __restrict__ table, int zdim, double inv_res, double* __restrict__ logw,
