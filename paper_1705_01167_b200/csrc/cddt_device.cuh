@@ -600,9 +600,16 @@ template <bool FRESH>
 __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, double y, int a,
                                                WinState& s, int cap, double* result) {
   const bool forward = a < c.S;
-  const SliceParam sp = c.slices[forward ? a : a - c.S];
-  const double xq = x * sp.cos_t + y * sp.sin_t;
+  // a forward direction is its slice's own direction (the same glibc cos/sin),
+  // so only backward queries read the slice record
   const double4 dir = c.dirs[a];
+  double cs = dir.x, sn = dir.y;
+  if (!forward) {
+    const double2 sl = __ldg(reinterpret_cast<const double2*>(c.slices + (a - c.S)));
+    cs = sl.x;
+    sn = sl.y;
+  }
+  const double xq = x * cs + y * sn;
   const float* __restrict__ v = c.zp + s.lo;
   const int n = (int)s.n, step = forward ? 1 : -1;
   Walker<true> wk;

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
 struct __align__(16) ContRecord {
   float x, y, t;
   uint32_t i, lo, n;
-  int32_t idx, cx, cy, pad;
+  int32_t idx, cx, cy, a;  // a: the query's direction index (not recomputed per pass)
   double wt;
 };
 
@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z),
                      __float_as_int(w1.w), __float_as_int(w2.x),
                      __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z)), 0.f};
+        a = __float_as_int(w2.y);
       } else {
         float4 w0, w1;
         ld256_cs(static_cast<const WalkRecord*>(in) + k, w0, w1);
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z), 0, 0, 0.0,
                      w1.w};
       }
-      a = direction_index(normalize_angle_2pi(double(ft)), c.K);
+      if (!CONT) a = direction_index(normalize_angle_2pi(double(ft)), c.K);
       double res;
       if (resume_windows<!CONT>(c, double(fx), double(fy), a, s, LAST ? 0x7fffffff : cap, &res))
         __stcs(out + qi, T(res));
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         __stcs(dst, make_float4(fx, fy, ft, __uint_as_float(qi)));
         __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
                                     __int_as_float(s.idx), __int_as_float(s.cx)));
-        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
+        __stcs(dst + 2, make_float4(__int_as_float(s.cy), __int_as_float(a),
                                     __int_as_float(__double2loint(s.t)),
                                     __int_as_float(__double2hiint(s.t))));
       } else {  // queue full: finish here
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
         __stcs(dst, w0);
         __stcs(dst + 1, make_float4(__uint_as_float(s.lo), __uint_as_float(s.n),
                                     __int_as_float(s.idx), __int_as_float(s.cx)));
-        __stcs(dst + 2, make_float4(__int_as_float(s.cy), 0.f,
+        __stcs(dst + 2, make_float4(__int_as_float(s.cy), __int_as_float(a),
                                     __int_as_float(__double2loint(s.t)),
                                     __int_as_float(__double2hiint(s.t))));
       } else {  // queue full: finish here
