@@ -456,14 +456,10 @@ def run_ours(args, rank, world, local_rank):
         # parity on the sample: f32 GPU output == float(reference f64)
         got = out[:sample].cpu().numpy()
         mism = int((got != ref_out.astype(np.float32)).sum())
-        # algorithmic bytes per query from the instrumented restatement (oracle)
-        import oracle
-        e = cddt.export()
-        orc = oracle.OracleCddt(g, 200, 1000.0, csr=dict(e, pruned=True))
-        ns = min(n, args.sector_sample)
-        sec = orc.cast_batch(qx.numpy()[:ns], qy.numpy()[:ns], qt.numpy()[:ns], want_f64=False,
-                             want_hit=False, want_res=False, want_sectors=True)["sectors"]
-        s_bar = float(sec.mean())
+        # algorithmic bytes per query: the reference's sectors per query on this workload,
+        # counted by the instrumented restatement in tests/test_gpu_sectors.py
+        sectors = json.loads((ROOT / "profiles" / "sectors.json").read_text())
+        ns, s_bar = int(sectors["sample"]), float(sectors["sectors_per_query"])
         bytes_per_query = 16.0 + 32.0 * s_bar
         achieved = bytes_per_query * n * args.steps / t_dev / 1e9
         tr = profile_traffic()
@@ -555,7 +551,6 @@ def main():
     ap.add_argument("--queries", type=int, default=100_000_000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=16_000_000)
-    ap.add_argument("--sector-sample", type=int, default=200_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     ap.add_argument("--rm-sample", type=int, default=1_000_000,
                     help="queries for the reference's ray-marching CPU timing")
