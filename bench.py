@@ -66,7 +66,7 @@ REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_powe
 
 
 class ClockSampler:
-    """nvidia-smi sampled every 100 ms while the timed region runs."""
+    """nvidia-smi sampled every 20 ms; summary() covers the samples after mark()."""
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
@@ -76,13 +76,22 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the timed region starts once samples flow (nvidia-smi takes a moment to start)
+            t0 = time.monotonic()
+            while not self.rows and time.monotonic() - t0 < 2.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.skip = len(self.rows)
         except OSError:
             self.proc = None
         return self
+
+    def mark(self):
+        """The timed region starts now: earlier samples are not reported."""
+        self.skip = len(self.rows)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -99,6 +108,9 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        # drop the samples taken before the timed region began (keep one if nothing else)
+        rows = self.rows[getattr(self, "skip", 0):] or self.rows[-1:]
+        self.rows = rows
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -400,10 +412,11 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        cddt.cast_batch(dx, dy, dt, out=out)
-    barrier()
     with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            cddt.cast_batch(dx, dy, dt, out=out)
+        barrier()
+        clk.mark()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
