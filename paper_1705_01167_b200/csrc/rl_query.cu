@@ -411,10 +411,29 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     const size_t b1 = std::max<size_t>(
         1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), kP1Threads, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
-    k_cast_near<T><<<sm_count() * pn, kWalkThreads, 0, st>>>(v, q, qn, uint32_t(n), qa, qn + 2,
-                                                             uint32_t(cap_a), out);
+    // the near-field kernel and window pass 0 read disjoint ends of the record
+    // queue and both append to queue A: they run side by side (fork / join)
+    struct Side {
+      cudaStream_t s = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    static thread_local Side side[64];
+    int dev = 0;
+    RL_CK(cudaGetDevice(&dev));
+    Side& sd = side[dev & 63];
+    if (!sd.s) {
+      RL_CK(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+      RL_CK(cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming));
+      RL_CK(cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming));
+    }
+    RL_CK(cudaEventRecord(sd.fork, st));
+    RL_CK(cudaStreamWaitEvent(sd.s, sd.fork, 0));
+    k_cast_near<T><<<sm_count() * pn, kWalkThreads, 0, sd.s>>>(v, q, qn, uint32_t(n), qa, qn + 2,
+                                                               uint32_t(cap_a), out);
+    RL_CK(cudaEventRecord(sd.join, sd.s));
     k_walk_pass<T, false, false><<<sm_count() * pw0, kWalkThreads, 0, st>>>(
         v, q, qn, uint32_t(n), kCaps[0], qa, qn + 2, uint32_t(cap_a), out);
+    RL_CK(cudaStreamWaitEvent(st, sd.join, 0));
     for (int p = 1; p < kPasses; p++) {  // queue p-1 -> queue p (A, B, A, ...)
       const bool from_a = (p & 1) != 0;
       k_walk_pass<T, true, false><<<sm_count() * pwc, kWalkThreads, 0, st>>>(
