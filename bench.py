@@ -497,15 +497,17 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                     "d2h_bytes_per_step": 4 * n, "steps": args.e2e_steps,
                     "path": "rl_cddt_cast_batch_host (pinned host buffers, 3-stream pipeline)"},
-            # per step: k_cast_defer_p1, k_cast_near, four k_walk_pass window passes
-            "gpu_launches": 6 * args.steps,
+            # per step: two pipelines (one per half of the batch) of k_cast_defer_p1,
+            # k_cast_near and four k_walk_pass window passes
+            "gpu_launches": 12 * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} hbm_gbs",
                          "algorithmic_bytes_per_query": bytes_per_query, "sectors_per_query": s_bar,
                          "sector_sample": ns,
-                         "kernel": "batched cast = k_cast_defer_p1 + k_cast_near + 4 x k_walk_pass (window "
-                                   "passes) back to back; timed per step",
+                         "kernel": "batched cast = 2 pipelines (halves of the batch, two streams) of "
+                                   "k_cast_defer_p1 + k_cast_near + 4 x k_walk_pass (window passes); "
+                                   "timed per step",
                          "gather_ceiling": gather},
             "cpu_baseline": {"value": sample / ref_dt, "unit": UNIT, "cores": threads,
                              "kind": "reference",

@@ -346,7 +346,8 @@ constexpr size_t kDeferMinQueries = size_t(1) << RL_DEFER_MIN_LOG2;
 // Dispatch of the batched cast kernels for the device-pointer entry points.
 template <class T>
 static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* out,
-                       int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st) {
+                       int32_t* hit, int64_t* rr, int32_t* ri, size_t n, cudaStream_t st,
+                       bool split = true) {
   const CddtView v = c->view();
   const bool small = n < (size_t(1) << 31);
 #ifndef RL_DEFER_MAX_LOG2
@@ -359,6 +360,38 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
       RL_TRY(launch_cast<T>(c, x + off, y + off, t + off, out + off, nullptr, nullptr, nullptr,
                             m, st));
     }
+    return RL_OK;
+  }
+  static const int parts = [] {
+    const char* e = std::getenv("RL_SPLIT_PARTS");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  if (split && parts > 1 && !rr && !ri && !hit && small && n >= kDeferMinQueries * parts) {
+    // two independent pipelines over the halves of the batch, on the caller's
+    // stream and a forked one: the late, thinly occupied window passes of one
+    // overlap the other's phase 1
+    struct Part {
+      cudaStream_t s = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+    };
+    static thread_local Part part[64];
+    int dev = 0;
+    RL_CK(cudaGetDevice(&dev));
+    Part& pp = part[dev & 63];
+    if (!pp.s) {
+      RL_CK(cudaStreamCreateWithFlags(&pp.s, cudaStreamNonBlocking));
+      RL_CK(cudaEventCreateWithFlags(&pp.fork, cudaEventDisableTiming));
+      RL_CK(cudaEventCreateWithFlags(&pp.join, cudaEventDisableTiming));
+    }
+    RL_CK(cudaEventRecord(pp.fork, st));
+    RL_CK(cudaStreamWaitEvent(pp.s, pp.fork, 0));
+    for (int k = 0; k < parts; k++) {  // chunks alternate between the two streams
+      const size_t a = n * size_t(k) / size_t(parts), b = n * size_t(k + 1) / size_t(parts);
+      RL_TRY(launch_cast<T>(c, x + a, y + a, t + a, out + a, nullptr, nullptr, nullptr, b - a,
+                            (k & 1) ? pp.s : st, false));
+    }
+    RL_CK(cudaEventRecord(pp.join, pp.s));
+    RL_CK(cudaStreamWaitEvent(st, pp.join, 0));
     return RL_OK;
   }
   if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
