@@ -169,29 +169,104 @@ def make_workload(n_queries: int, rank: int, on_gpu: bool = True):
     return g, qx, qy, qt, np
 
 
-def reference_cpu(g, qx, qy, qt, sample: int, snapshot: bytes | None, threads: int):
-    """Time the unmodified reference (oracle/_ref) on `sample` queries with all
-    threads. With `snapshot` the reference loads that structure through its own
-    deserialize_cddt; otherwise it builds its own (unpruned) CDDT."""
+REF_PCDDT = ROOT / "oracle" / "_ref" / "cfg3_pcddt.rlc"
+
+
+def reference_structure(g):
+    """The config-3 PCDDT as the unmodified reference built it
+    (scripts/make_ref_pcddt.py: Cddt::Cddt + Cddt::prune, ~12 min
+    single-threaded), loaded through the reference's own deserialize_cddt
+    (cddt.cpp:502-579); its sha256 is committed in oracle/cfg3_pcddt.sha256.
+    Returns (handle, snapshot bytes, description, same_config). Without the
+    snapshot the reference builds an unpruned CDDT (its prune is outside any
+    run budget) and same_config is False."""
+    import hashlib
+
     import oracle
     oracle.build(ref=True)
     if not oracle.ref_available():
         raise RuntimeError("oracle/_ref/librangelib_ref.so not built")
-    t0 = time.perf_counter()
-    if snapshot is not None:
-        ref = oracle.RefCddt.deserialize(snapshot)
-        how = "GPU-built PCDDT loaded via the reference's deserialize_cddt"
-    else:
-        ref = oracle.RefCddt(g, 200, 1000.0, prune=False)
-        how = ("reference-built CDDT (unpruned: the reference's single-threaded prune of this map "
-               "takes minutes, outside the run budget)")
-    setup = time.perf_counter() - t0
+    want = (ROOT / "oracle" / "cfg3_pcddt.sha256").read_text().split()[0]
+    if REF_PCDDT.exists():
+        blob = REF_PCDDT.read_bytes()
+        if hashlib.sha256(blob).hexdigest() != want:
+            raise RuntimeError(f"{REF_PCDDT} does not match oracle/cfg3_pcddt.sha256")
+        return (oracle.RefCddt.deserialize(blob), blob,
+                "the reference-built PCDDT (scripts/make_ref_pcddt.py) loaded via its own "
+                "deserialize_cddt", True)
+    return (oracle.RefCddt(g, 200, 1000.0, prune=False), None,
+            "a reference-built unpruned CDDT (oracle/_ref/cfg3_pcddt.rlc absent: the reference's "
+            "single-threaded prune of this map takes ~12 min)", False)
+
+
+def reference_cpu(ref, qx, qy, qt, sample: int, threads: int, sample1: int):
+    """Time the unmodified reference's Cddt::cast on `sample` queries with all
+    host threads (wall clock; a std::thread partition over the const cast, safe
+    per SPEC.md:341) and on `sample1` queries on one thread, timed by thread cpu
+    time as the reference's own benchmark does (proj/src/bench.cpp:52-121)."""
     xs, ys, ts = qx[:sample], qy[:sample], qt[:sample]
     ref.cast_batch(xs[:10000], ys[:10000], ts[:10000], want_res=False, threads=threads)
     t0 = time.perf_counter()
     r = ref.cast_batch(xs, ys, ts, want_res=False, threads=threads)
     dt = time.perf_counter() - t0
-    return ref, r["out64"], dt, setup, how
+    _, sec1 = ref.cast_batch_cpu1(qx[:sample1], qy[:sample1], qt[:sample1])
+    return r["out64"], dt, sample1 / sec1
+
+
+def reference_cpu_configs(threads: int, mcl_iterations: int = 10) -> dict:
+    """The reference's CPU paths beside BASELINE configs 1, 2 and 4 (the
+    unmodified rangelib in oracle/_ref, through its public API):
+      config 1: Cddt build + 100k casts (one thread, thread cpu time; and all threads)
+      config 2: sensor_update (mcl.cpp:58-120), 2,500 particles x 61 paired beams
+      config 4: Mcl::step (mcl.cpp:189-201), 40,000 particles x 61 beams, a bounded
+                run of `mcl_iterations` steps (its own MclStepResult.seconds)
+    The reference's sensor model is the analytic beam_likelihood: it has no
+    likelihood-table path, so configs 2 and 4 run the analytic model here."""
+    import numpy as np
+
+    import oracle
+    from paper_1705_01167_b200 import synth
+    out = {}
+    g1 = synth.rect_map()
+    t0 = time.perf_counter()
+    r1 = oracle.RefCddt(g1, 108, 300.0)
+    build1 = time.perf_counter() - t0
+    qx, qy, qt = synth.free_queries(g1, 100_000, seed=7)
+    _, sec1 = r1.cast_batch_cpu1(qx, qy, qt)
+    t0 = time.perf_counter()
+    r1.cast_batch(qx, qy, qt, want_res=False, threads=threads)
+    dtn = time.perf_counter() - t0
+    out["config1"] = {"build_s": build1, "casts_per_s_1thread": 100_000 / sec1,
+                      "casts_per_s_all_threads": 100_000 / dtn, "threads": threads}
+    del r1
+    g2 = synth.maze_map()
+    r2 = oracle.RefCddt(g2, 120, 500.0)
+    x, y, t = synth.free_pose(g2, 10, seed=5)
+    px, py, pt = synth.particles(x, y, t, 2500, 10.0, 0.1, seed=9)
+    scan = synth.scan(g2, x, y, t, 61, 4.71238898038469, 500.0, 8.0, 0.05, seed=13)
+    params = oracle.beam_params(sigma_hit=8.0, z_max=500.0)
+    r2.sensor_update(px, py, pt, scan, 4.71238898038469, params, paired=True)
+    reps, t0 = 5, time.perf_counter()
+    for _ in range(reps):
+        r2.sensor_update(px, py, pt, scan, 4.71238898038469, params, paired=True)
+    ms2 = (time.perf_counter() - t0) / reps * 1e3
+    out["config2"] = {"ms_per_sensor_update": ms2, "casts_per_s": 2500 * 61 / ms2 * 1e3,
+                      "threads": 1, "model": "analytic beam_likelihood (no table path in the "
+                                               "reference)", "paired_casts": True}
+    x0, y0, t0_ = synth.free_pose(g2, 15, seed=8)
+    pose, odo = synth.trajectory(g2, x0, y0, t0_, mcl_iterations, 1.0, 15.0, seed=4)
+    scans = np.stack([synth.scan(g2, *pose[k + 1], 61, 4.71238898038469, 500.0, 8.0, 0.05,
+                                 seed=1000 + k) for k in range(mcl_iterations)])
+    sec, _ = r2.mcl_run(40_000, 5, (x0, y0, t0_), 10.0, 0.1, (1.0, 0.0, 0.0, 0.02), params,
+                        4.71238898038469, np.asarray(odo, np.float64), scans)
+    out["config4"] = {"ms_per_update_p50": float(np.median(sec)) * 1e3,
+                      "ms_per_update_mean": float(np.mean(sec)) * 1e3,
+                      "iterations_timed": mcl_iterations, "threads": 1,
+                      "extrapolated_1000_iterations_s": float(np.mean(sec)) * 1000,
+                      "model": "analytic beam_likelihood (no table path in the reference)",
+                      "what": "rangelib::Mcl::step (motion, paired-cast sensor model, estimate, "
+                              "resampling), its own MclStepResult.seconds"}
+    return out
 
 
 def gather_ceiling(device: int) -> dict:
@@ -261,15 +336,28 @@ def pf_update_timing(iterations: int, device: int, group=None):
     for k in range(5):
         f.step(*odo[k], scans[k])
     torch.cuda.synchronize()
-    times, errs = [], []
+    # throughput: the iterations issued back to back (Mcl.step never waits for
+    # the device), an event after each; per-update time = consecutive events
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(iterations + 1)]
+    evs[0].record()
+    results = []
     for k in range(iterations):
+        results.append(f.step(*odo[k], scans[k]))
+        evs[k + 1].record()
+    evs[-1].synchronize()
+    times = [evs[k].elapsed_time(evs[k + 1]) for k in range(iterations)]
+    errs = [float(np.hypot(r.estimate.x - pose[k + 1][0], r.estimate.y - pose[k + 1][1]))
+            for k, r in enumerate(results)]
+    # latency: one update at a time, its estimate read back before the next
+    lat = []
+    for k in range(min(iterations, 100)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         r = f.step(*odo[k], scans[k])
+        r.estimate
         e1.record()
         e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-        errs.append(float(np.hypot(r.estimate.x - pose[k + 1][0], r.estimate.y - pose[k + 1][1])))
+        lat.append(e0.elapsed_time(e1))
     times = np.array(times)
     world = 1
     if group is not None:
@@ -285,11 +373,16 @@ def pf_update_timing(iterations: int, device: int, group=None):
                            if world > 1 else ""),
             "iterations": iterations, "ms_per_update_p50": float(np.median(times)),
             "ms_per_update_mean": float(times.mean()), "ms_per_update_p99":
-            float(np.percentile(times, 99)), "casts_per_update": 40_000 * 61,
+            float(np.percentile(times, 99)),
+            "timing": "iterations issued back to back (no host sync), CUDA events between "
+                      "updates; ms_per_update_synchronous_p50: one update at a time with its "
+                      "estimate read back (host launch latency included)",
+            "ms_per_update_synchronous_p50": float(np.median(lat)),
+            "casts_per_update": 40_000 * 61,
             "median_position_error_px": float(np.median(errs[10:]))}
 
 
-def other_configs(device: int, rounds: int = 20):
+def other_configs(device: int, rounds: int = 1000):
     """BASELINE configs 1, 2 and 5 on one GPU (timings only; parity for each
     is in tests/test_gpu_*.py)."""
     import numpy as np
@@ -354,26 +447,55 @@ def other_configs(device: int, rounds: int = 20):
              dict(x=px, y=py, theta=pt, weight=np.zeros_like(px)).items()}
     spec = rl.ScanSpec(61, 4.71238898038469)
     ms2 = ev_time(lambda: rl.sensor_update(parts, m2, scan, spec, beam, table=table), 200)
+    flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
+    ms2a = ev_time(lambda: rl.sensor_update(parts, m2, scan, spec, beam, table=table,
+                                            degenerate=flag), 200)
     out["config2"] = {"workload": "2000x2000 maze, theta_disc=120, max_range=500, 2500 particles x "
-                                  "61 beams, 501x501 table", "ms_per_sensor_update": ms2,
-                      "casts_per_s": 2500 * 61 / ms2 * 1e3}
-    # config 5: 2000x2000 maze, theta_disc 108; rounds of 50 random 3x3 edits + 1M queries
+                                  "61 beams, 501x501 table",
+                      "ms_per_sensor_update": ms2a, "casts_per_s": 2500 * 61 / ms2a * 1e3,
+                      "timing": "200 updates issued back to back through sensor_update(..., "
+                                "degenerate=<device flag>) (rl_sensor_update_async), CUDA events",
+                      "ms_per_sensor_update_synchronous": ms2,
+                      "synchronous": "sensor_update returning the reference's bool (flag read "
+                                     "back every update)"}
+    # config 5: 2000x2000 maze, theta_disc 108; 1,000 rounds of 50 random 3x3
+    # edits + 1M queries, the round sequence of tests/golden/cfg5_rounds.json
+    # (reference digests after every round; tests/test_gpu_cfg5.py checks every
+    # one, the bench checks the final structure and casts)
+    import hashlib
+    gold = json.loads((ROOT / "tests" / "golden" / "cfg5_rounds.json").read_text())
     c5 = rl.Cddt(rl.OccupancyGrid.from_array(g2), rl.RangeMethodConfig(0.0, 108), device=device)
     q5 = [torch.from_numpy(a).cuda(device) for a in synth.free_queries(g2, 1_000_000, seed=31)]
     o5 = torch.empty_like(q5[0])
+    edits = [synth.block_edits(2000, 2000, 50, seed=gold["seed0"] + r) for r in range(rounds)]
     upd, qry = [], []
     for r in range(rounds):
-        xy, occ = synth.block_edits(2000, 2000, 50, seed=9000 + r)
+        xy, occ = edits[r]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         c5.set_occupancy_batch(xy, occ)
         upd.append(time.perf_counter() - t0)
-        qry.append(ev_time(lambda: c5.cast_batch(*q5, out=o5), 3))
+        qry.append(ev_time(lambda: c5.cast_batch(*q5, out=o5), 1))
+    parity = None
+    if rounds == len(gold["rounds"]):
+        last = gold["rounds"][-1]
+        e = c5.export()
+        dig = [hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+               for a in (e["zp"], e["row_off"], e["membership"])]
+        o64 = c5.cast_batch_f64(*(a.double() for a in q5))
+        parity = (dig == [last["zp"], last["row_off"], last["membership"]]
+                  and hashlib.sha256(o64.cpu().numpy().tobytes()).hexdigest() == last["casts"])
     out["config5"] = {"workload": "2000x2000 maze, theta_disc=108, rounds of 50 random 3x3 "
                                   "insert/remove blocks + 1M queries", "rounds": rounds,
                       "ms_per_update_round_p50": 1e3 * float(np.median(upd)),
+                      "ms_per_update_round_mean": 1e3 * float(np.mean(upd)),
                       "ms_per_1M_queries_p50": float(np.median(qry)),
-                      "zero_points_after": c5.zero_point_count()}
+                      "zero_points_after": c5.zero_point_count(),
+                      "parity_vs_reference_final_round": parity,
+                      "parity_note": "zero points, row offsets, membership and 1M f64 casts after "
+                                     "the last round equal the reference's digests "
+                                     "(tests/golden/cfg5_rounds.json); every round is checked "
+                                     "by tests/test_gpu_cfg5.py"}
     return out
 
 
@@ -463,9 +585,12 @@ def run_ours(args, rank, world, local_rank):
         peak, peak_kind = measured_hbm_peak()
         sample = min(n, args.cpu_sample)
         threads = os.cpu_count() or 1
-        snap = rl.serialize_cddt(cddt)
-        ref, ref_out, ref_dt, _, how = reference_cpu(g, qx.numpy(), qy.numpy(), qt.numpy(), sample,
-                                                     snap, threads)
+        ref, ref_blob, how, same = reference_structure(g)
+        # the GPU-built PCDDT, in the reference's snapshot format, byte for byte
+        structure_equal = ref_blob is not None and rl.serialize_cddt(cddt) == ref_blob
+        ref_out, ref_dt, ref_1t = reference_cpu(ref, qx.numpy(), qy.numpy(), qt.numpy(), sample,
+                                                threads, min(n, args.cpu_sample_1t))
+        cpu_cfgs = reference_cpu_configs(threads, args.ref_mcl_iterations)
         # parity on the sample: f32 GPU output == float(reference f64)
         got = out[:sample].cpu().numpy()
         mism = int((got != ref_out.astype(np.float32)).sum())
@@ -513,7 +638,14 @@ def run_ours(args, rank, world, local_rank):
                              "kind": "reference",
                              "sample": f"{sample} queries of this workload on {how}; "
                                        f"{cpu_model()}",
+                             "same_config": same,
+                             "gpu_structure_bytes_equal_reference": structure_equal,
+                             "value_1thread": ref_1t,
+                             "sample_1thread": f"{min(n, args.cpu_sample_1t)} queries on one "
+                                               "thread, thread cpu time (the reference's "
+                                               "bench.cpp:52-121 clock)",
                              "parity_mismatches": mism,
+                             "configs": cpu_cfgs,
                              "ray_march": ray_march_cpu(g, qx.numpy(), qy.numpy(), qt.numpy(),
                                                         min(n, args.rm_sample), threads)},
             "clocks": clk.summary(),
@@ -523,15 +655,14 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_reference(args):
-    """--impl reference: the unmodified reference on the host cores, rank 0 only."""
+    """--impl reference: the unmodified reference on the host cores, rank 0 only,
+    on the same structure as our arm (the reference-built config-3 PCDDT)."""
     n = args.ref_sample
     g, qx, qy, qt, np = make_workload(n, 0, on_gpu=False)
     threads = os.cpu_count() or 1
-    import oracle
-    oracle.build(ref=True)
     t0 = time.perf_counter()
-    ref = oracle.RefCddt(g, 200, 1000.0, prune=False)
-    build_s = time.perf_counter() - t0
+    ref, _, how, same = reference_structure(g)
+    load_s = time.perf_counter() - t0
     xs, ys, ts = qx.numpy(), qy.numpy(), qt.numpy()
     for _ in range(args.warmup):
         ref.cast_batch(xs, ys, ts, want_res=False, threads=threads)
@@ -540,6 +671,8 @@ def run_reference(args):
         ref.cast_batch(xs, ys, ts, want_res=False, threads=threads)
     dt = time.perf_counter() - t0
     value = n * args.steps / dt
+    _, sec1 = ref.cast_batch_cpu1(xs[:args.cpu_sample_1t], ys[:args.cpu_sample_1t],
+                                  ts[:args.cpu_sample_1t])
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
@@ -547,14 +680,41 @@ def run_reference(args):
         "data": "synthetic (seeded BASELINE config-3 map and query stream)",
         "config": dict(workload_config(args.queries), parallelism="host threads"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{n} queries per step (bounded sample of the 100M-query step) "
-                                   f"on the reference's own Cddt (unpruned; its single-threaded "
-                                   f"prune of this map takes minutes), build {build_s:.1f} s; "
-                                   f"{cpu_model()}",
+                         "sample": f"{n} queries per step (a bounded sample of the 100M-query "
+                                   f"step) on {how} (load {load_s:.1f} s); {cpu_model()}",
+                         "same_config": same,
+                         "value_1thread": args.cpu_sample_1t / sec1,
+                         "sample_1thread": f"{args.cpu_sample_1t} queries on one thread, thread "
+                                           "cpu time (the reference's bench.cpp:52-121 clock)",
                          "ray_march": ray_march_cpu(g, xs, ys, ts, min(n, args.rm_sample),
                                                     threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N ranks (one per GPU, NCCL, 127.0.0.1), as the
+    driver's own torchrun launch would. Refuses when fewer than N GPUs are
+    visible rather than timing fewer GPUs than asked for."""
+    import socket
+
+    if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+            return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the init lines show nranks / transports
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -567,6 +727,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=16_000_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
+    ap.add_argument("--cpu-sample-1t", type=int, default=2_000_000,
+                    help="queries for the reference's one-thread timing")
+    ap.add_argument("--ref-mcl-iterations", type=int, default=20,
+                    help="reference Mcl::step iterations timed beside config 4")
     ap.add_argument("--rm-sample", type=int, default=1_000_000,
                     help="queries for the reference's ray-marching CPU timing")
     ap.add_argument("--pf-iterations", type=int, default=1000)
@@ -574,7 +738,15 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         if rank != 0:
             return 0
@@ -583,9 +755,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        dev = local_rank % torch.cuda.device_count()
-        torch.cuda.set_device(dev)
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: host-logic checks only
+        if backend == "nccl" and local_rank >= torch.cuda.device_count():
+            print(f"bench.py: rank {rank} has LOCAL_RANK {local_rank} but only "
+                  f"{torch.cuda.device_count()} GPUs are visible", file=sys.stderr)
+            return 2
+        dev = local_rank % torch.cuda.device_count()  # gloo only: ranks may share a GPU
+        torch.cuda.set_device(dev)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:

@@ -257,6 +257,62 @@ int rl_mcl_step(rl_cddt *c, double *x, double *y, double *theta, double *w, size
                 const rl_beam_params_t *params, const float *table, int32_t zdim, double inv_res,
                 uint64_t seed, uint64_t iteration, double *estimate, void *stream);
 
+/* ---- asynchronous forms (no host synchronisation; for pipelined and
+ * multi-GPU drivers). `stream` must be non-NULL; successive sensor /
+ * particle-filter calls on one handle must use one stream (they share the
+ * handle's workspace in stream order). ---- */
+
+/* rl_sensor_update without the read-back: the degenerate flag (1 where the
+ * reference's sensor_update returns false, mcl.cpp:114-117) is written to the
+ * device int32 *degenerate. */
+int rl_sensor_update_async(rl_cddt *c, const double *px, const double *py, const double *pt,
+                           size_t n, const double *scan, int32_t nbeams, double fov,
+                           const rl_beam_params_t *params, const float *table, int32_t zdim,
+                           double inv_res, double *logw, double *weight, int32_t *degenerate,
+                           void *stream);
+
+/* rl_mcl_step without the read-back: the estimate (Mcl::estimate,
+ * mcl.cpp:176-187, computed on the device) goes to the device buffer
+ * estimate_dev = {x, y, theta, degenerate (0.0 / 1.0)}. */
+int rl_mcl_step_async(rl_cddt *c, double *x, double *y, double *theta, double *w, size_t n,
+                      double odo_dx, double odo_dy, double odo_dtheta, const double *scan,
+                      int32_t nbeams, double fov, const rl_motion_noise_t *noise,
+                      const rl_beam_params_t *params, const float *table, int32_t zdim,
+                      double inv_res, uint64_t seed, uint64_t iteration, double *estimate_dev,
+                      void *stream);
+
+/* ---- the sharded Mcl::step (one process per GPU). Per step:
+ *   rl_pf_shard_sensor -> all-reduce MAX(local_max) -> rl_pf_weights ->
+ *   all-reduce SUM(moments) -> rl_pf_normalize -> rl_pf_estimate ->
+ *   all-gather {x, y, theta, w} -> rl_resample_gathered
+ * with no host synchronisation between the stages. ---- */
+
+/* motion_update (mcl.cpp:42-56; skipped when noise is NULL) fused with the
+ * sensor model's log-weights (mcl.cpp:64-103) for this rank's shard
+ * (global indices [index_offset, index_offset + n)); *local_max (device) =
+ * max over the shard's log-weights, -inf for an empty shard. */
+int rl_pf_shard_sensor(rl_cddt *c, double *x, double *y, double *theta, size_t n,
+                       uint64_t index_offset, double odo_dx, double odo_dy, double odo_dtheta,
+                       const rl_motion_noise_t *noise, uint64_t seed, uint64_t iteration,
+                       const double *scan, int32_t nbeams, double fov,
+                       const rl_beam_params_t *params, const float *table, int32_t zdim,
+                       double inv_res, double *logw, double *local_max, void *stream);
+
+/* Mcl::estimate (mcl.cpp:176-187) from the all-reduced moments of
+ * rl_pf_weights and the flag of rl_pf_normalize (may be NULL: not degenerate),
+ * on the device: estimate_dev = {x, y, theta, degenerate}. */
+int rl_pf_estimate(const double *moments, const int32_t *degenerate, uint64_t n_total,
+                   double *estimate_dev, void *stream);
+
+/* resample_low_variance (mcl.cpp:122-142) read straight from an all-gather
+ * of per-rank shards: gathered = [world][4][n_local] doubles, rank-major, each
+ * rank's block {x[n_local], y[n_local], theta[n_local], w[n_local]} (the
+ * rank-concatenated output of ncclAllGather). Same comb and output slots as
+ * rl_resample_low_variance over the concatenated set. */
+int rl_resample_gathered(const double *gathered, size_t n_local, int32_t world, size_t out_begin,
+                         size_t out_count, double *ox, double *oy, double *otheta, double *ow,
+                         uint64_t seed, uint64_t iteration, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -115,6 +115,9 @@ def ref_lib() -> C.CDLL:
         h.ref_rm_create.restype = _P
         h.ref_rm_destroy.argtypes = [_P]
         h.ref_rm_cast_batch.argtypes = [_P, _P, _P, _P, _sz, _P, C.c_int]
+        h.ref_cast_batch_cpu1.argtypes = [_P, _P, _P, _P, _sz, _P, _P]
+        h.ref_mcl_run.argtypes = [_P, C.c_int, C.c_uint64, _d, _d, _d, _d, _d, _P, _P, C.c_int, _d,
+                                  C.c_int, _P, _P, _P, _P]
         _ref = h
     return _ref
 
@@ -319,12 +322,40 @@ class RefCddt(_Base):
                                    out.ctypes.data)
         return out
 
-    def bench(self, random_mode: bool, n: int = 0, seed: int = 1, stride: int = 4):
-        """The reference's run_random/grid_benchmark: (queries, checksum, map_id)."""
-        out = np.zeros(2)
+    def bench(self, random_mode: bool, n: int = 0, seed: int = 1, stride: int = 4,
+              with_seconds: bool = False):
+        """The reference's run_random/grid_benchmark: (queries, checksum, map_id)
+        [, total thread-cpu seconds]."""
+        out = np.zeros(3)
         mid = C.create_string_buffer(17)
         ref_lib().ref_bench(self._h, 1 if random_mode else 0, n, seed, stride, out.ctypes.data, mid)
-        return int(out[0]), float(out[1]), mid.value.decode()
+        r = (int(out[0]), float(out[1]), mid.value.decode())
+        return r + (float(out[2]),) if with_seconds else r
+
+    def cast_batch_cpu1(self, qx, qy, qt):
+        """Casts on the calling thread, timed by thread cpu time (the
+        reference's benchmark clock): (f64 ranges, cpu seconds)."""
+        qx, qy, qt = _a(qx, np.float32), _a(qy, np.float32), _a(qt, np.float32)
+        out = np.empty(qx.size)
+        sec = np.zeros(1)
+        ref_lib().ref_cast_batch_cpu1(self._h, qx.ctypes.data, qy.ctypes.data, qt.ctypes.data,
+                                      qx.size, out.ctypes.data, sec.ctypes.data)
+        return out, float(sec[0])
+
+    def mcl_run(self, n, seed, pose0, sigma_xy, sigma_th, noise, params, fov, odo, scans):
+        """The reference's Mcl (init_gaussian + step per odometry/scan row):
+        (per-step MclStepResult.seconds, per-step estimates [k, 3])."""
+        odo = _a(odo, np.float64).reshape(-1, 3)
+        scans = _a(scans, np.float64)
+        it, nb = scans.shape
+        nz, p = _a(noise, np.float64), _a(params, np.float64)
+        sec, est = np.zeros(it), np.zeros((it, 3))
+        st = ref_lib().ref_mcl_run(self._h, n, seed, *pose0, sigma_xy, sigma_th, nz.ctypes.data,
+                                   p.ctypes.data, nb, fov, it, odo.ctypes.data, scans.ctypes.data,
+                                   sec.ctypes.data, est.ctypes.data)
+        if st:
+            raise RuntimeError(f"reference Mcl failed ({st})")
+        return sec, est
 
     def lut_build(self, theta_disc):
         i = self.info()

@@ -10,6 +10,8 @@
 // Used by tests/ to pin the C restatement (oracle/cddt_oracle.c) and the GPU
 // path, and by bench.py --impl reference / cpu_baseline as the reference's
 // own CPU implementation timed on the host cores.
+#include <time.h>
+
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -312,7 +314,59 @@ void ref_bench(void* hp, int random_mode, size_t n, uint64_t seed, int stride, d
                                 : run_grid_benchmark(view, r.c.grid(), cfg, stride);
   out[0] = double(rep.queries);
   out[1] = rep.checksum;
+  out[2] = rep.total_seconds;  // summed per-batch thread cpu time (bench.cpp:52-121)
   std::strncpy(id, rep.map_id.c_str(), 17);
+}
+
+// Cddt::cast over f32 queries on the calling thread, timed like the
+// reference's own benchmark (run_batches, proj/src/bench.cpp:52-121): thread
+// cpu time, which does not advance while the core is taken away.
+void ref_cast_batch_cpu1(void* hp, const float* qx, const float* qy, const float* qt, size_t n,
+                         double* out, double* cpu_seconds) {
+  const RefCddt& r = *static_cast<RefCddt*>(hp);
+  timespec a{}, b{};
+  clock_gettime(CLOCK_THREAD_CPUTIME_ID, &a);
+  for (size_t i = 0; i < n; i++) out[i] = r.c.cast(RayQuery(double(qx[i]), double(qy[i]), double(qt[i])));
+  clock_gettime(CLOCK_THREAD_CPUTIME_ID, &b);
+  *cpu_seconds = double(b.tv_sec - a.tv_sec) + 1e-9 * double(b.tv_nsec - a.tv_nsec);
+}
+
+// The reference's own particle filter (rangelib::Mcl, proj/src/mcl.cpp:156-201)
+// over a CddtMethod-equivalent view (paired casts on): init_gaussian, then
+// `iters` steps with odometry odo[3k..3k+2] and scan scans[k*nb..]; per step
+// its MclStepResult.seconds and estimate. noise = MotionNoise fields, p =
+// BeamModelParams fields. The reference's sensor model is the analytic
+// beam_likelihood (it has no table path).
+int ref_mcl_run(void* hp, int n, uint64_t seed, double x0, double y0, double t0, double sxy,
+                double sth, const double* noise, const double* p, int nb, double fov, int iters,
+                const double* odo, const double* scans, double* seconds, double* est) {
+  const RefCddt& r = *static_cast<RefCddt*>(hp);
+  try {
+    CddtView view(r.c, true);
+    MclConfig cfg;
+    cfg.particle_count = n;
+    cfg.seed = seed;
+    cfg.scan.beam_count = nb;
+    cfg.scan.fov = fov;
+    cfg.motion.trans_per_trans = noise[0];
+    cfg.motion.trans_per_rot = noise[1];
+    cfg.motion.rot_per_rot = noise[2];
+    cfg.motion.rot_per_trans = noise[3];
+    cfg.beam = beam_params(p);
+    Mcl mcl(view, cfg);
+    mcl.init_gaussian(x0, y0, t0, sxy, sth);
+    for (int k = 0; k < iters; k++) {
+      std::vector<double> sc(scans + size_t(k) * nb, scans + size_t(k + 1) * nb);
+      MclStepResult res = mcl.step(odo[3 * k], odo[3 * k + 1], odo[3 * k + 2], sc);
+      seconds[k] = res.seconds;
+      est[3 * k] = res.estimate.x;
+      est[3 * k + 1] = res.estimate.y;
+      est[3 * k + 2] = res.estimate.theta;
+    }
+    return RS_OK;
+  } catch (...) {
+    return RS_EOTHER;
+  }
 }
 
 // Ray marching baseline (make_method(ray_march), proj/src/methods.cpp:55-72).

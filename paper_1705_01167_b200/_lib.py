@@ -96,6 +96,21 @@ _SIG = {
                               _P, C.c_int32, C.c_double, C.POINTER(rl_motion_noise_t),
                               C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double,
                               C.c_uint64, C.c_uint64, _P, _P]),
+    "rl_mcl_step_async": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, C.c_double, C.c_double,
+                                    C.c_double, _P, C.c_int32, C.c_double,
+                                    C.POINTER(rl_motion_noise_t), C.POINTER(rl_beam_params_t), _P,
+                                    C.c_int32, C.c_double, C.c_uint64, C.c_uint64, _P, _P]),
+    "rl_sensor_update_async": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,
+                                         C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double,
+                                         _P, _P, _P, _P]),
+    "rl_pf_estimate": (C.c_int, [_P, _P, C.c_uint64, _P, _P]),
+    "rl_resample_gathered": (C.c_int, [_P, C.c_size_t, C.c_int32, C.c_size_t, C.c_size_t, _P, _P,
+                                       _P, _P, C.c_uint64, C.c_uint64, _P]),
+    "rl_pf_shard_sensor": (C.c_int, [_P, _P, _P, _P, C.c_size_t, C.c_uint64, C.c_double,
+                                     C.c_double, C.c_double, C.POINTER(rl_motion_noise_t),
+                                     C.c_uint64, C.c_uint64, _P, C.c_int32, C.c_double,
+                                     C.POINTER(rl_beam_params_t), _P, C.c_int32, C.c_double, _P,
+                                     _P, _P]),
 }
 
 _lib = None

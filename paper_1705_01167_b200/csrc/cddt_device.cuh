@@ -57,16 +57,23 @@ __host__ __device__ __forceinline__ double fmax_std(double a, double b) { return
 
 __device__ __forceinline__ long iround(double v) { return (long)ceil(v - 0.5); }  // raycast.hpp:17
 
-// a / d correctly rounded, given r = RN(1/d): q0 = RN(a r) is within one ulp
-// of a/d and the FMA residual a - d q0 is exact, so RN(q0 + (a - d q0) r) =
-// RN(a/d) (Markstein's theorem; every operand here is far from overflow and
-// the subnormal range). Three FP64 operations instead of the ~30-instruction
-// IEEE division sequence; checked bit-for-bit against IEEE division on the
-// walker's and direction_index's operands by tests/fast_div_check.c.
+// a / d correctly rounded, given r = RN(1/d) (host IEEE division).
+// Markstein's theorem: if q is a faithful rounding of a/d (within one ulp)
+// and r = RN(1/d), the FMA residual e = a - d q is exact and RN(q + e r) =
+// RN(a/d) — barring overflow and subnormals, which the walker's and
+// direction_index's operands never reach (|a| < 2^16; |d| >= sin(2pi/K), far
+// above the subnormal range for any usable K).
+// q0 = RN(a r) alone is NOT always faithful (|q0 - a/d| can reach ~2 ulp at
+// the top of a binade), so one correction step first makes it faithful:
+//   q1 = RN(q0 + RN(a - d q0) r):  |q1 - a/d| <= 1/2 ulp + 2 ulp * 2^-52 < 1 ulp,
+// and the second step rounds correctly. Five FP64 operations instead of the
+// ~30-instruction IEEE division sequence; tests/fast_div_check.c also checks
+// it bit for bit against IEEE division on the walker's operand distribution
+// (float and f64 origins, cell centres, lattice-adjacent origins).
 __device__ __forceinline__ double div_rn(double a, double d, double r) {
   const double q0 = __dmul_rn(a, r);
-  const double e = fma(-d, q0, a);
-  return fma(e, r, q0);
+  const double q1 = fma(fma(-d, q0, a), r, q0);
+  return fma(fma(-d, q1, a), r, q1);
 }
 
 __device__ __forceinline__ double normalize_angle_2pi(double t) {  // raycast.hpp:20-25

@@ -46,20 +46,67 @@ int sm_count() {
   return n;
 }
 
-// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
-// pool; with an unbounded release threshold freed blocks stay reserved, so
-// steady-state allocations cost nothing and never synchronise.
-void retain_pool() {
-  static thread_local int done_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+// Stream-ordered scratch (cudaMallocAsync) comes from a memory pool owned by
+// this library, one per device, never from the device's default pool, whose
+// settings the host application (e.g. PyTorch) may rely on. While any handle
+// on the device is alive the pool keeps freed blocks reserved (release
+// threshold UINT64_MAX), so steady-state allocations cost nothing and never
+// synchronise; when the last handle on the device is destroyed the pool is
+// trimmed to zero and the memory goes back to the driver (trim_pools).
+namespace {
+struct PoolSlot {
+  cudaMemPool_t pool = nullptr;
+  int live_handles = 0;
+};
+std::mutex g_pool_mu;
+PoolSlot g_pools[64];
+}  // namespace
+
+static int pool_for(int dev, cudaMemPool_t* out) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  PoolSlot& ps = g_pools[dev & 63];
+  if (!ps.pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    RL_CK(cudaMemPoolCreate(&ps.pool, &props));
     uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    RL_CK(cudaMemPoolSetAttribute(ps.pool, cudaMemPoolAttrReleaseThreshold, &keep));
   }
-  done_dev = dev;
+  *out = ps.pool;
+  return RL_OK;
+}
+
+int scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  RL_CK(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  RL_TRY(pool_for(dev, &pool));
+  RL_CK(cudaMallocFromPoolAsync(p, bytes, pool, st));
+  return RL_OK;
+}
+
+int scratch_free(void* p, cudaStream_t st) {
+  RL_CK(cudaFreeAsync(p, st));
+  return RL_OK;
+}
+
+void handle_opened(int dev) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  g_pools[dev & 63].live_handles++;
+}
+
+// the last handle on `dev` is gone: return the pool's reserved memory (after
+// the device is idle, so no stream-ordered free is still pending)
+void handle_closed(int dev) {
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  PoolSlot& ps = g_pools[dev & 63];
+  if (--ps.live_handles > 0 || !ps.pool) return;
+  ps.live_handles = 0;
+  cudaDeviceSynchronize();
+  cudaMemPoolTrimTo(ps.pool, 0);
 }
 
 int finish(const rl_cddt* c, void* s) {
@@ -497,6 +544,8 @@ int create_handle(int32_t device, rl_cddt** out, rl_cddt** keep) {
     set_error("cudaStreamCreate: %s", cudaGetErrorString(e));
     return RL_ECUDA;
   }
+  handle_opened(device);
+  c->counted = true;
   *keep = c;
   return RL_OK;
 }
@@ -562,7 +611,8 @@ int rl_cddt_destroy(rl_cddt* c) {
   if (!c) return RL_OK;
   {
     DeviceGuard guard(c->dev);
-    if (c->stream) cudaStreamSynchronize(c->stream);
+    // casts may still run on caller streams (rl_cddt_cast_batch is async)
+    cudaDeviceSynchronize();
     c->flags.release();
     c->rowbits.release();
     c->row_off.release();
@@ -581,6 +631,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     if (c->pf_host) cudaFreeHost(c->pf_host);
     if (c->host_small) cudaFreeHost(c->host_small);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->counted) handle_closed(c->dev);
   }
   delete c;
   return RL_OK;
@@ -589,6 +640,7 @@ int rl_cddt_destroy(rl_cddt* c) {
 int rl_cddt_prune(rl_cddt* c) {
   if (!c) return RL_EINVAL;
   DeviceGuard guard(c->dev);
+  RL_TRY(quiesce(c));  // casts queued on caller streams read the structure being replaced
   return prune_structure(c);
 }
 

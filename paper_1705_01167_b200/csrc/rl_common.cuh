@@ -98,6 +98,7 @@ struct DeviceGuard {
 // membership (small: w*h bytes) that drive incremental edits.
 struct rl_cddt {
   int dev = 0;
+  bool counted = false;  // registered with the scratch pool (handle_opened)
   cudaStream_t stream = nullptr;
   int w = 0, h = 0, K = 0, S = 0;
   double max_range = 0.0, resolution = 0.05;
@@ -161,7 +162,19 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
-void retain_pool();                     // the current device's default pool keeps freed memory
+// stream-ordered scratch from the library's own per-device pool (rl_cddt.cu)
+int scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+int scratch_free(void* p, cudaStream_t st);
+void handle_opened(int dev);  // pool bookkeeping: live handles per device
+void handle_closed(int dev);
+// Structure changes (prune, set_occupancy*) rewrite arrays that casts already
+// queued on caller streams may still read: wait for all work on the device
+// first. Casts are asynchronous on any stream, so only a device-wide
+// synchronisation orders them before the change.
+inline int quiesce(const rl_cddt*) {
+  RL_CK(cudaDeviceSynchronize());
+  return RL_OK;
+}
 // 16 pinned u32 for small device->host read-backs (a pageable destination
 // would add a staging copy to every synchronous step)
 inline int host_small(rl_cddt* c, uint32_t** out) {

@@ -57,7 +57,7 @@ extern "C" int rl_diag_gather(const void* buf, size_t bytes, size_t loads, void*
   const uint32_t rounds =
       uint32_t(std::max<size_t>(1, loads / (threads * kGatherInFlight)));
   uint32_t* sink = nullptr;
-  RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&sink), sizeof(uint32_t), st));
+  RL_TRY(scratch_alloc(reinterpret_cast<void**>(&sink), sizeof(uint32_t), st));
   cudaEvent_t e0, e1;
   RL_CK(cudaEventCreate(&e0));
   RL_CK(cudaEventCreate(&e1));
@@ -72,7 +72,7 @@ extern "C" int rl_diag_gather(const void* buf, size_t bytes, size_t loads, void*
   RL_CK(cudaEventElapsedTime(&f, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  RL_CK(cudaFreeAsync(sink, st));
+  RL_TRY(scratch_free(sink, st));
   RL_CK(cudaStreamSynchronize(st));
   *ms = double(f);
   *issued = uint64_t(threads) * kGatherInFlight * rounds;

@@ -23,6 +23,7 @@
 //                        tile prefix | low-variance comb | copy back
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <chrono>
 #include <cmath>
@@ -143,7 +144,31 @@ struct ScanSmem {
   typename cub::BlockScan<double, kPfThreads>::TempStorage scan;
 };
 
-__device__ __forceinline__ void scan_tile(const double* __restrict__ w, size_t n, size_t tile,
+// Particle sets as the scan and the comb read them: four plain arrays, or the
+// rank-concatenated block an all-gather of per-rank {x, y, theta, w} shards
+// leaves ([world][4][n_local], rank-major), read in place.
+struct PlainSet {
+  const double *x, *y, *t, *w;
+  __device__ __forceinline__ double gx(size_t i) const { return x[i]; }
+  __device__ __forceinline__ double gy(size_t i) const { return y[i]; }
+  __device__ __forceinline__ double gt(size_t i) const { return t[i]; }
+  __device__ __forceinline__ double gw(size_t i) const { return __ldcg(w + i); }
+};
+struct GatheredSet {
+  const double* base;
+  size_t n_local;
+  __device__ __forceinline__ double at(int comp, size_t i) const {
+    const size_t r = i / n_local, j = i - r * n_local;
+    return base[(r * 4 + size_t(comp)) * n_local + j];
+  }
+  __device__ __forceinline__ double gx(size_t i) const { return at(0, i); }
+  __device__ __forceinline__ double gy(size_t i) const { return at(1, i); }
+  __device__ __forceinline__ double gt(size_t i) const { return at(2, i); }
+  __device__ __forceinline__ double gw(size_t i) const { return at(3, i); }
+};
+
+template <class Set>
+__device__ __forceinline__ void scan_tile(const Set& ps, size_t n, size_t tile,
                                           bool normalise, double s, bool bad,
                                           double* __restrict__ local,
                                           double* __restrict__ tile_total, ScanSmem& sm) {
@@ -154,7 +179,7 @@ __device__ __forceinline__ void scan_tile(const double* __restrict__ w, size_t n
     const size_t i = base + k;
     double a = 0.0;
     if (i < n) {
-      const double wi = __ldcg(w + i);  // may come from another block of this grid
+      const double wi = ps.gw(i);  // may come from another block of this grid
       a = normalise ? (bad ? 1.0 / double(n) : wi / s) : wi;
     }
     v[k] = a;
@@ -189,11 +214,10 @@ __device__ __forceinline__ void tile_prefix(const double* __restrict__ tile_tota
 
 // slot m takes the first particle i with cumulative weight >= r + m/n,
 // capped at n-1 (the sequential comb of mcl.cpp:130-140)
+template <class Set>
 __device__ __forceinline__ void comb_slots(const double* __restrict__ local,
                                            const double* __restrict__ tile_excl,
-                                           const double* __restrict__ x,
-                                           const double* __restrict__ y,
-                                           const double* __restrict__ t, size_t n,
+                                           const Set& ps, size_t n,
                                            size_t out_begin, size_t out_count,
                                            double* __restrict__ ox, double* __restrict__ oy,
                                            double* __restrict__ ot, double* __restrict__ ow,
@@ -216,9 +240,9 @@ __device__ __forceinline__ void comb_slots(const double* __restrict__ local,
       }
     }
     const size_t i = lo < n ? lo : n - 1;
-    ox[k] = x[i];
-    oy[k] = y[i];
-    ot[k] = t[i];
+    ox[k] = ps.gx(i);
+    oy[k] = ps.gy(i);
+    ot[k] = ps.gt(i);
     ow[k] = 1.0 / double(n);
   }
 }
@@ -262,13 +286,14 @@ __global__ void k_normalize(double* __restrict__ w, size_t n, const double* __re
 
 // tile scan of already-normalised weights; the last tile to finish writes the
 // tile prefix
+template <class Set>
 __global__ void __launch_bounds__(kPfThreads) k_tile_scan(
-    const double* __restrict__ w, size_t n, double* __restrict__ local,
+    Set ps, size_t n, double* __restrict__ local,
     double* __restrict__ tile_total, double* __restrict__ tile_excl,
     unsigned* __restrict__ ticket) {
   __shared__ ScanSmem sm;
   __shared__ bool last;
-  scan_tile(w, n, blockIdx.x, false, 1.0, false, local, tile_total, sm);
+  scan_tile(ps, n, blockIdx.x, false, 1.0, false, local, tile_total, sm);
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -280,13 +305,46 @@ __global__ void __launch_bounds__(kPfThreads) k_tile_scan(
   if (threadIdx.x == 0) *ticket = 0;
 }
 
+template <class Set>
 __global__ void k_comb(const double* __restrict__ local, const double* __restrict__ tile_excl,
-                       const double* __restrict__ x, const double* __restrict__ y,
-                       const double* __restrict__ t, size_t n, size_t out_begin,
+                       Set ps, size_t n, size_t out_begin,
                        size_t out_count, double* __restrict__ ox, double* __restrict__ oy,
                        double* __restrict__ ot, double* __restrict__ ow, uint64_t seed,
                        uint64_t iter) {
-  comb_slots(local, tile_excl, x, y, t, n, out_begin, out_count, ox, oy, ot, ow, seed, iter);
+  comb_slots(local, tile_excl, ps, n, out_begin, out_count, ox, oy, ot, ow, seed, iter);
+}
+
+// Mcl::estimate (mcl.cpp:176-187) from the weight moments of the step:
+// normalised weights w_i = e_i / S make the sums the e-moments divided by S; a
+// degenerate reset gives uniform weights 1/n. est = {x, y, theta, degenerate}.
+__device__ __forceinline__ void estimate_from_moments(const double* m, bool deg, uint64_t n,
+                                                      double* __restrict__ est) {
+  double sx, sy, sc, ss, sw;
+  if (deg) {
+    const double inv = 1.0 / double(n);
+    sx = m[6] * inv;
+    sy = m[7] * inv;
+    sc = m[8] * inv;
+    ss = m[9] * inv;
+    sw = m[5] * inv;
+  } else {
+    sx = m[1] / m[0];
+    sy = m[2] / m[0];
+    sc = m[3] / m[0];
+    ss = m[4] / m[0];
+    sw = 1.0;
+  }
+  if (!(sw > 0.0)) sw = 1.0;
+  est[0] = sx / sw;
+  est[1] = sy / sw;
+  est[2] = normalize_angle_2pi(atan2(ss, sc));
+  est[3] = deg ? 1.0 : 0.0;
+}
+
+__global__ void k_estimate(const double* __restrict__ moments,
+                           const int32_t* __restrict__ degenerate, uint64_t n,
+                           double* __restrict__ est) {
+  estimate_from_moments(moments, degenerate && *degenerate != 0, n, est);
 }
 
 // ---- the fused step after the sensor model: one cooperative kernel ----
@@ -297,6 +355,7 @@ struct FinishArgs {
   size_t n;
   double *partial, *local, *tile_total, *tile_excl, *nxyzw;
   Moments* out;
+  double* est;  // optional device {x, y, theta, degenerate} (the asynchronous step)
   uint64_t seed, iter;
 };
 
@@ -320,19 +379,22 @@ __global__ void __launch_bounds__(kPfThreads, 2) k_pf_finish(FinishArgs a) {
   const double S = mom[0];
   const bool bad = degenerate_sum(S);
   if (blockIdx.x == 0 && threadIdx.x < 10) a.out->m[threadIdx.x] = mom[threadIdx.x];
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.out->degenerate = bad ? 1 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out->degenerate = bad ? 1 : 0;
+    if (a.est) estimate_from_moments(mom, bad, n, a.est);
+  }
   // 3. normalised tile scans
   __shared__ ScanSmem sm;
   const size_t tiles = (n + kScanTile - 1) / kScanTile;
   for (size_t j = blockIdx.x; j < tiles; j += gridDim.x) {
-    scan_tile(a.w, n, j, true, S, bad, a.local, a.tile_total, sm);
+    scan_tile(PlainSet{a.x, a.y, a.t, a.w}, n, j, true, S, bad, a.local, a.tile_total, sm);
     __syncthreads();
   }
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x < 32) tile_prefix(a.tile_total, tiles, a.tile_excl);
   grid.sync();
   // 4. comb into the scratch set, then copy back over the caller's arrays
-  comb_slots(a.local, a.tile_excl, a.x, a.y, a.t, n, 0, n, a.nxyzw, a.nxyzw + n,
+  comb_slots(a.local, a.tile_excl, PlainSet{a.x, a.y, a.t, a.w}, n, 0, n, a.nxyzw, a.nxyzw + n,
              a.nxyzw + 2 * n, a.nxyzw + 3 * n, a.seed, a.iter);
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.gmax_key = 0;  // ready for the next step
@@ -347,7 +409,8 @@ __global__ void __launch_bounds__(kPfThreads, 2) k_pf_finish(FinishArgs a) {
 
 __global__ void k_key_to_double(const unsigned long long* __restrict__ key,
                                 double* __restrict__ out) {
-  *out = order_key_value(*key);
+  const unsigned long long k = *key;
+  *out = k ? order_key_value(k) : -CUDART_INF;  // key 0: nothing was scored
 }
 
 __global__ void k_copy_back(const double* __restrict__ src, double* __restrict__ x,
@@ -417,13 +480,12 @@ int rl_motion_update(double* x, double* y, double* theta, size_t n, uint64_t ind
 int rl_pf_max(const double* logw, size_t n, double* out, void* stream) {
   if (!logw || !out || n == 0) return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool();
   size_t bytes = 0;
   cub::DeviceReduce::Max(nullptr, bytes, logw, out, int(n), s);
   void* tmp = nullptr;  // stream-ordered scratch: no synchronisation needed
-  RL_CK(cudaMallocAsync(&tmp, bytes, s));
+  RL_TRY(scratch_alloc(&tmp, bytes, s));
   RL_CK(cub::DeviceReduce::Max(tmp, bytes, logw, out, int(n), s));
-  RL_CK(cudaFreeAsync(tmp, s));
+  RL_TRY(scratch_free(tmp, s));
   if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
@@ -432,7 +494,6 @@ int rl_pf_weights(const double* logw, const double* gmax, const double* x, const
                   const double* theta, size_t n, double* w, double* moments, void* stream) {
   if (!logw || !gmax || !x || !y || !theta || !w || !moments) return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool();
   if (n == 0) {
     RL_CK(cudaMemsetAsync(moments, 0, 10 * sizeof(double), s));
     RL_CK(cudaStreamSynchronize(s));
@@ -440,12 +501,12 @@ int rl_pf_weights(const double* logw, const double* gmax, const double* x, const
   }
   const int nb = moment_blocks(n);
   double* partial = nullptr;  // stream-ordered scratch: partials | ticket
-  RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&partial), 8 * (size_t(nb) * 10 + 1), s));
+  RL_TRY(scratch_alloc(reinterpret_cast<void**>(&partial), 8 * (size_t(nb) * 10 + 1), s));
   unsigned* ticket = reinterpret_cast<unsigned*>(partial + size_t(nb) * 10);
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   k_weights<<<nb, kPfThreads, 0, s>>>(logw, gmax, x, y, theta, n, w, partial, ticket, moments);
   RL_CK(cudaGetLastError());
-  RL_CK(cudaFreeAsync(partial, s));
+  RL_TRY(scratch_free(partial, s));
   if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
@@ -468,27 +529,33 @@ int rl_resample_low_variance(const double* x, const double* y, const double* the
   if (!x || !y || !theta || !w || !ox || !oy || !otheta || !ow || out_begin + out_count > n)
     return RL_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool();
   const size_t T = scan_tiles(n);
   double* local = nullptr;  // stream-ordered scratch: local[n] | tile_total[T] | tile_excl[T] | ticket
-  RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&local), 8 * (n + 2 * T + 1), s));
+  RL_TRY(scratch_alloc(reinterpret_cast<void**>(&local), 8 * (n + 2 * T + 1), s));
   double *tile_total = local + n, *tile_excl = tile_total + T;
   unsigned* ticket = reinterpret_cast<unsigned*>(tile_excl + T);
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
-  k_tile_scan<<<int(T), kPfThreads, 0, s>>>(w, n, local, tile_total, tile_excl, ticket);
-  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, x, y, theta, n, out_begin, out_count,
+  const PlainSet ps{x, y, theta, w};
+  k_tile_scan<<<int(T), kPfThreads, 0, s>>>(ps, n, local, tile_total, tile_excl, ticket);
+  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, ps, n, out_begin, out_count,
                                           ox, oy, otheta, ow, seed, iteration);
   RL_CK(cudaGetLastError());
-  RL_CK(cudaFreeAsync(local, s));
+  RL_TRY(scratch_free(local, s));
   if (!stream) RL_CK(cudaStreamSynchronize(s));
   return RL_OK;
 }
 
-int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size_t n,
-                double odo_dx, double odo_dy, double odo_dtheta, const double* scan,
-                int32_t nbeams, double fov, const rl_motion_noise_t* noise,
-                const rl_beam_params_t* params, const float* table, int32_t zdim, double inv_res,
-                uint64_t seed, uint64_t iteration, double* estimate, void* stream) {
+}  // extern "C"
+
+// The fused Mcl::step. Synchronous form (est_dev == nullptr): the moments come
+// back to the host and `estimate` is computed there. Asynchronous form: the
+// estimate is computed on the device into est_dev and nothing waits.
+static int mcl_step_impl(rl_cddt* c, double* x, double* y, double* theta, double* w, size_t n,
+                         double odo_dx, double odo_dy, double odo_dtheta, const double* scan,
+                         int32_t nbeams, double fov, const rl_motion_noise_t* noise,
+                         const rl_beam_params_t* params, const float* table, int32_t zdim,
+                         double inv_res, uint64_t seed, uint64_t iteration, double* estimate,
+                         double* est_dev, void* stream) {
   if (!c || !noise || !scan || nbeams <= 0 || (n && (!x || !y || !theta || !w))) return RL_EINVAL;
   if (n > (1ull << 32)) {
     set_error("motion_update: particle index exceeds the 32-bit RNG counter");
@@ -527,6 +594,7 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
   fa.tile_excl = fa.tile_total + T;
   fa.partial = fa.tile_excl + T;
   fa.out = mom;
+  fa.est = est_dev;
   fa.seed = seed;
   fa.iter = iteration;
 
@@ -561,14 +629,21 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
     k_weights<<<nbw, kPfThreads, 0, st>>>(fa.logw, gmax, x, y, theta, n, w, fa.partial,
                                           &ctl->ticket, mom->m);
     k_normalize<<<blocks(n), 256, 0, st>>>(w, n, mom->m, n, &mom->degenerate);
-    k_tile_scan<<<int(T), kPfThreads, 0, st>>>(w, n, fa.local, fa.tile_total, fa.tile_excl,
+    const PlainSet ps{x, y, theta, w};
+    k_tile_scan<<<int(T), kPfThreads, 0, st>>>(ps, n, fa.local, fa.tile_total, fa.tile_excl,
                                                &ctl->ticket);
-    k_comb<<<blocks(n), 256, 0, st>>>(fa.local, fa.tile_excl, x, y, theta, n, 0, n, fa.nxyzw,
+    if (est_dev) k_estimate<<<1, 1, 0, st>>>(mom->m, &mom->degenerate, n, est_dev);
+    k_comb<<<blocks(n), 256, 0, st>>>(fa.local, fa.tile_excl, ps, n, 0, n, fa.nxyzw,
                                       fa.nxyzw + n, fa.nxyzw + 2 * n, fa.nxyzw + 3 * n, seed,
                                       iteration);
     k_copy_back<<<blocks(n), 256, 0, st>>>(fa.nxyzw, x, y, theta, w, n, &ctl->gmax_key);
   }
   RL_CK(cudaGetLastError());
+  if (est_dev) {
+    // the key is reset by the step itself, in stream order
+    c->pf_ctl_clean = true;
+    return RL_OK;
+  }
 #ifdef RL_PF_TRACE
   cudaEventRecord(ev[2], st);
   auto host_t1 = std::chrono::steady_clock::now();
@@ -621,6 +696,101 @@ int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size
     estimate[2] = th;
   }
   return deg ? RL_EDEGENERATE : RL_OK;
+}
+
+extern "C" {
+
+int rl_mcl_step(rl_cddt* c, double* x, double* y, double* theta, double* w, size_t n,
+                double odo_dx, double odo_dy, double odo_dtheta, const double* scan,
+                int32_t nbeams, double fov, const rl_motion_noise_t* noise,
+                const rl_beam_params_t* params, const float* table, int32_t zdim, double inv_res,
+                uint64_t seed, uint64_t iteration, double* estimate, void* stream) {
+  return mcl_step_impl(c, x, y, theta, w, n, odo_dx, odo_dy, odo_dtheta, scan, nbeams, fov, noise,
+                       params, table, zdim, inv_res, seed, iteration, estimate, nullptr, stream);
+}
+
+int rl_mcl_step_async(rl_cddt* c, double* x, double* y, double* theta, double* w, size_t n,
+                      double odo_dx, double odo_dy, double odo_dtheta, const double* scan,
+                      int32_t nbeams, double fov, const rl_motion_noise_t* noise,
+                      const rl_beam_params_t* params, const float* table, int32_t zdim,
+                      double inv_res, uint64_t seed, uint64_t iteration, double* estimate_dev,
+                      void* stream) {
+  if (!estimate_dev || !stream) {
+    set_error("rl_mcl_step_async needs a device estimate buffer and a stream");
+    return RL_EINVAL;
+  }
+  if (n == 0) return RL_OK;
+  return mcl_step_impl(c, x, y, theta, w, n, odo_dx, odo_dy, odo_dtheta, scan, nbeams, fov, noise,
+                       params, table, zdim, inv_res, seed, iteration, nullptr, estimate_dev,
+                       stream);
+}
+
+int rl_pf_estimate(const double* moments, const int32_t* degenerate, uint64_t n_total,
+                   double* estimate_dev, void* stream) {
+  if (!moments || !estimate_dev || n_total == 0) return RL_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_estimate<<<1, 1, 0, s>>>(moments, degenerate, n_total, estimate_dev);
+  RL_CK(cudaGetLastError());
+  if (!stream) RL_CK(cudaStreamSynchronize(s));
+  return RL_OK;
+}
+
+int rl_resample_gathered(const double* gathered, size_t n_local, int32_t world, size_t out_begin,
+                         size_t out_count, double* ox, double* oy, double* otheta, double* ow,
+                         uint64_t seed, uint64_t iteration, void* stream) {
+  if (world <= 0 || n_local == 0 || out_count == 0) return world > 0 ? RL_OK : RL_EINVAL;
+  const size_t n = n_local * size_t(world);
+  if (!gathered || !ox || !oy || !otheta || !ow || out_begin + out_count > n) return RL_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t T = scan_tiles(n);
+  double* local = nullptr;  // stream-ordered scratch: local[n] | tile_total[T] | tile_excl[T] | ticket
+  RL_TRY(scratch_alloc(reinterpret_cast<void**>(&local), 8 * (n + 2 * T + 1), s));
+  double *tile_total = local + n, *tile_excl = tile_total + T;
+  unsigned* ticket = reinterpret_cast<unsigned*>(tile_excl + T);
+  RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+  const GatheredSet ps{gathered, n_local};
+  k_tile_scan<<<int(T), kPfThreads, 0, s>>>(ps, n, local, tile_total, tile_excl, ticket);
+  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, ps, n, out_begin, out_count, ox, oy,
+                                          otheta, ow, seed, iteration);
+  RL_CK(cudaGetLastError());
+  RL_TRY(scratch_free(local, s));
+  if (!stream) RL_CK(cudaStreamSynchronize(s));
+  return RL_OK;
+}
+
+int rl_pf_shard_sensor(rl_cddt* c, double* x, double* y, double* theta, size_t n,
+                       uint64_t index_offset, double odo_dx, double odo_dy, double odo_dtheta,
+                       const rl_motion_noise_t* noise, uint64_t seed, uint64_t iteration,
+                       const double* scan, int32_t nbeams, double fov,
+                       const rl_beam_params_t* params, const float* table, int32_t zdim,
+                       double inv_res, double* logw, double* local_max, void* stream) {
+  if (!c || !local_max || !scan || nbeams <= 0 || (n && (!x || !y || !theta || !logw)))
+    return RL_EINVAL;
+  if (index_offset + n > (1ull << 32)) {
+    set_error("motion_update: particle index exceeds the 32-bit RNG counter");
+    return RL_EINVAL;
+  }
+  if (!table && (!params || !(params->z_max > 0.0))) {
+    set_error("beam model z_max must be positive");  // mcl.cpp:13
+    return RL_EINVAL;
+  }
+  std::lock_guard<std::mutex> lock(c->mu);
+  DeviceGuard guard(c->dev);
+  cudaStream_t st = pick_stream(c, stream);
+  unsigned long long* key = nullptr;  // stream-ordered scratch: the max key
+  RL_TRY(scratch_alloc(reinterpret_cast<void**>(&key), sizeof *key, st));
+  RL_CK(cudaMemsetAsync(key, 0, sizeof *key, st));
+  if (n) {
+    MotionArgs mot{};
+    if (noise) mot = motion_args(odo_dx, odo_dy, odo_dtheta, noise, seed, iteration, index_offset);
+    RL_TRY(sensor_logw_launch(c, x, y, theta, n, scan, nbeams, fov, params, table, zdim, inv_res,
+                              logw, noise ? &mot : nullptr, key, st));
+  }
+  // an empty shard reports -inf (key 0 decodes to NaN; the max all-reduce must ignore it)
+  k_key_to_double<<<1, 1, 0, st>>>(key, local_max);
+  RL_CK(cudaGetLastError());
+  RL_TRY(scratch_free(key, st));
+  return finish(c, stream);
 }
 
 }  // extern "C"

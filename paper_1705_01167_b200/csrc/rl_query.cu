@@ -398,8 +398,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     // stream-ordered scratch: concurrent batches on other streams (e.g. the
     // pipelined host path) each get their own queue; the pool keeps the
     // memory reserved, so steady-state allocation is free
-    retain_pool();
-    // workspace: counters | n walk records (windows up from 0, near field down
+      // workspace: counters | n walk records (windows up from 0, near field down
     // from n-1) | continuation queues A and B (the window passes alternate)
     // (RL_CDDT_CONT_CAP overrides the queue capacity: a test hook for the
     // queue-full path)
@@ -419,7 +418,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     const size_t cap_a = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_A_DIV, size_t(1) << 16);
     const size_t cap_b = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_B_DIV, size_t(1) << 16);
     uint8_t* ws = nullptr;
-    RL_CK(cudaMallocAsync(reinterpret_cast<void**>(&ws),
+    RL_TRY(scratch_alloc(reinterpret_cast<void**>(&ws),
                           256 + sizeof(WalkRecord) * n + sizeof(ContRecord) * (cap_a + cap_b),
                           st));
     unsigned* qn = reinterpret_cast<unsigned*>(ws);  // windows, near, one per capped pass
@@ -487,7 +486,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
       fprintf(stderr, "\n");
     }
 #endif
-    RL_CK(cudaFreeAsync(ws, st));
+    RL_TRY(scratch_free(ws, st));
     return RL_OK;
   }
   if (rr || ri) {

@@ -309,12 +309,22 @@ int rl_beam_table(const rl_beam_params_t* p, int32_t zdim, double inv_res, float
   return RL_OK;
 }
 
-int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const double* pt, size_t n,
-                     const double* scan, int32_t nbeams, double fov,
-                     const rl_beam_params_t* params, const float* table, int32_t zdim,
-                     double inv_res, double* logw, double* weight, void* stream) {
+}  // extern "C"
+
+// sensor_update: synchronous (degenerate_dev == nullptr: the flag is read back
+// and returned as RL_EDEGENERATE) or asynchronous (the flag is written to
+// degenerate_dev on the device and nothing waits).
+static int sensor_update_impl(rl_cddt* c, const double* px, const double* py, const double* pt,
+                              size_t n, const double* scan, int32_t nbeams, double fov,
+                              const rl_beam_params_t* params, const float* table, int32_t zdim,
+                              double inv_res, double* logw, double* weight,
+                              int32_t* degenerate_dev, void* stream) {
   RL_TRY(check_sensor_args(c, px, py, pt, n, scan, nbeams, params, table, zdim, inv_res));
-  if (n == 0) return RL_OK;
+  if (n == 0) {
+    if (degenerate_dev)
+      RL_CK(cudaMemsetAsync(degenerate_dev, 0, sizeof(int32_t), pick_stream(c, stream)));
+    return RL_OK;
+  }
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
   cudaStream_t st = pick_stream(c, stream);
@@ -330,11 +340,11 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   if (c->ws.n < need) RL_TRY(c->ws.alloc(need));
   uint8_t* base = c->ws.p;
   unsigned long long* key = reinterpret_cast<unsigned long long*>(base);
-  int* d_flag = reinterpret_cast<int*>(base + 8);
+  int* d_flag = degenerate_dev ? degenerate_dev : reinterpret_cast<int*>(base + 8);
   double* d_logw = logw ? logw : reinterpret_cast<double*>(base + 64);
   double* d_w = weight ? weight : reinterpret_cast<double*>(base + 64 + 8 * n);
   double* partial = reinterpret_cast<double*>(base + 64 + 16 * n);
-  RL_CK(cudaMemsetAsync(key, 0, 16, st));
+  RL_CK(cudaMemsetAsync(key, 0, 8, st));
   RL_TRY(sensor_logw_launch(c, const_cast<double*>(px), const_cast<double*>(py),
                             const_cast<double*>(pt), n, scan, nbeams, fov, params, table, zdim,
                             inv_res, d_logw, nullptr, key, st));
@@ -346,11 +356,35 @@ int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const doubl
   void* args[] = {&d_logw, &key, &d_w, &nn, &partial, &d_flag};
   RL_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sensor_normalize), dim3(nblk),
                                     dim3(256), args, 0, st));
+  if (degenerate_dev) return RL_OK;
   uint32_t* hs = nullptr;
   RL_TRY(host_small(c, &hs));
   RL_CK(cudaMemcpyAsync(hs, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
   return hs[0] ? RL_EDEGENERATE : RL_OK;
+}
+
+extern "C" {
+
+int rl_sensor_update(rl_cddt* c, const double* px, const double* py, const double* pt, size_t n,
+                     const double* scan, int32_t nbeams, double fov,
+                     const rl_beam_params_t* params, const float* table, int32_t zdim,
+                     double inv_res, double* logw, double* weight, void* stream) {
+  return sensor_update_impl(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
+                            logw, weight, nullptr, stream);
+}
+
+int rl_sensor_update_async(rl_cddt* c, const double* px, const double* py, const double* pt,
+                           size_t n, const double* scan, int32_t nbeams, double fov,
+                           const rl_beam_params_t* params, const float* table, int32_t zdim,
+                           double inv_res, double* logw, double* weight, int32_t* degenerate,
+                           void* stream) {
+  if (!degenerate || !stream) {
+    set_error("rl_sensor_update_async needs a device flag and a stream");
+    return RL_EINVAL;
+  }
+  return sensor_update_impl(c, px, py, pt, n, scan, nbeams, fov, params, table, zdim, inv_res,
+                            logw, weight, degenerate, stream);
 }
 
 }  // extern "C"

@@ -420,6 +420,7 @@ int rl_cddt_set_occupancy_batch(rl_cddt* c, const int32_t* xy, const uint8_t* oc
     }
   }
   DeviceGuard guard(c->dev);
+  if (valid) RL_TRY(quiesce(c));  // casts queued on caller streams read the rows being merged
   RL_TRY(apply_edits(c, xy, occupied, valid));
   if (valid < n) {
     set_error("cddt: cell outside the grid");  // cddt.cpp:334

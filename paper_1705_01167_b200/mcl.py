@@ -2,7 +2,7 @@
 rangelib/mcl.hpp:101-127, proj/src/mcl.cpp:156-201) with particles resident in
 HBM and every per-particle loop a kernel of librl_cddt.so.
 
-Single GPU: one C-ABI call per step (rl_mcl_step). Across GPUs (Mcl(...,
+Single GPU: one C-ABI call per step (rl_mcl_step_async). Across GPUs (Mcl(...,
 group=<torch.distributed process group>) with world_size > 1): particles are sharded, the map
 and CDDT are replicated on every GPU, and the step runs stage by stage with two
 exchanges over NCCL — the weight-sum all-reduce (max log-weight, then the
@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import RL_EDEGENERATE, check, lib, rl_motion_noise_t, torch_stream
+from ._lib import check, lib, rl_motion_noise_t, torch_stream
 from .rangelib import BeamModelParams, CddtMethod, ScanSpec, kTwoPi, normalize_angle_2pi
 
 
@@ -54,11 +54,41 @@ class PoseEstimate:
     theta: float = 0.0
 
 
-@dataclass
 class MclStepResult:
-    estimate: PoseEstimate
-    seconds: float = 0.0
-    degenerate: bool = False
+    """The result of Mcl::step (mcl.cpp:189-201): the pose estimate after the
+    sensor update (Mcl::estimate, mcl.cpp:176-187) and whether the weights were
+    degenerate and reset (sensor_update returned false).
+
+    The estimate is computed on the GPU and copied back into pinned host memory
+    asynchronously, so a step never waits for the device: reading `estimate`
+    or `degenerate` waits for that copy (`ready()` polls it). `seconds` is the
+    host time spent issuing the step."""
+
+    def __init__(self, host=None, event=None, seconds: float = 0.0,
+                 estimate: PoseEstimate | None = None, degenerate: bool = False):
+        self._host, self._event, self.seconds = host, event, seconds
+        self._est, self._deg = estimate, degenerate
+
+    def ready(self) -> bool:
+        return self._est is not None or self._event is None or self._event.query()
+
+    def _resolve(self) -> None:
+        if self._est is None:
+            if self._event is not None:
+                self._event.synchronize()
+            h = self._host.tolist()
+            self._est, self._deg = PoseEstimate(h[0], h[1], h[2]), bool(h[3])
+            self._host = self._event = None
+
+    @property
+    def estimate(self) -> PoseEstimate:
+        self._resolve()
+        return self._est
+
+    @property
+    def degenerate(self) -> bool:
+        self._resolve()
+        return self._deg
 
 
 def _p(t):
@@ -97,20 +127,23 @@ class Mcl:
         self.n_local = n // self.world
         self.offset = self.rank * self.n_local
         f64 = dict(dtype=torch.float64, device=self.dev)
-        self.x = torch.zeros(self.n_local, **f64)
-        self.y = torch.zeros(self.n_local, **f64)
-        self.theta = torch.zeros(self.n_local, **f64)
-        self.weight = torch.full((self.n_local,), 1.0 / n, **f64)
+        # this rank's particles as the rows of one [4, n_local] block {x, y, theta, w}:
+        # the block is what the resampling all-gather sends, with no packing copy
+        self.pblock = torch.zeros((4, self.n_local), **f64)
+        self.x, self.y, self.theta, self.weight = self.pblock.unbind(0)
+        self.weight.fill_(1.0 / n)
         self.iteration = 0
-        self._est = PoseEstimate()
+        self._last: MclStepResult | None = None
         self._scan_dev = torch.empty(cfg.scan.beam_count, **f64)
         self._bp = self.cfg.beam.c()
         self._noise = cfg.motion.c()
-        if True:  # stage buffers for the sharded path
-            self.logw = torch.empty(self.n_local, **f64)
-            self.gmax = torch.empty(1, **f64)
-            self.moments = torch.empty(10, **f64)
-            self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.est_dev = torch.zeros(4, **f64)  # {x, y, theta, degenerate} of the last step
+        # stage buffers of the sharded path
+        self.logw = torch.empty(self.n_local, **f64)
+        self.gmax = torch.empty(1, **f64)
+        self.moments = torch.empty(10, **f64)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.gathered = torch.empty((self.world * 4, self.n_local), **f64)
 
     # ---- Mcl::init_gaussian (mcl.cpp:165-174), seeded, shard-independent ----
     def init_gaussian(self, x, y, theta, sigma_xy, sigma_theta):
@@ -143,10 +176,16 @@ class Mcl:
         return {k: getattr(self, k).cpu().numpy() for k in ("x", "y", "theta", "weight")}
 
     def estimate(self) -> PoseEstimate:
-        return self._est
+        """Mcl::estimate after the last step (waits for it)."""
+        return self._last.estimate if self._last is not None else PoseEstimate()
 
     # ---- Mcl::step (mcl.cpp:189-201) ----
     def step(self, odo_dx, odo_dy, odo_dtheta, scan) -> MclStepResult:
+        """One filter step, issued without waiting for the device: motion,
+        sensor model, normalisation, estimate and resampling are queued on the
+        current stream (single GPU: two kernels, rl_mcl_step_async; sharded:
+        the stages with NCCL exchanges between them). The returned result
+        resolves its estimate when read."""
         import torch
         if len(scan) != self.cfg.scan.beam_count:
             raise ValueError("scan length does not match beam count")  # mcl.cpp:61-62
@@ -154,46 +193,52 @@ class Mcl:
         if isinstance(scan, torch.Tensor):
             self._scan_dev.copy_(scan, non_blocking=True)
         else:
-            self._scan_dev.copy_(torch.from_numpy(np.ascontiguousarray(scan, np.float64)))
-        stream = torch_stream(self.dev) if self.dev.type == "cuda" else None
+            # through pinned memory: a pageable host->device copy would wait for the stream
+            src = torch.from_numpy(np.ascontiguousarray(scan, np.float64))
+            if self.dev.type == "cuda":
+                src = src.pin_memory()
+            self._scan_dev.copy_(src, non_blocking=True)
+        cuda = self.dev.type == "cuda"
+        stream = torch_stream(self.dev) if cuda else None
         it = self.iteration
         self.iteration += 1
         if self.world == 1 and self.stages is None:
-            est = (C.c_double * 3)()
-            st = check(lib().rl_mcl_step(
+            check(lib().rl_mcl_step_async(
                 self.cddt.handle, _p(self.x), _p(self.y), _p(self.theta), _p(self.weight),
                 self.n_local, odo_dx, odo_dy, odo_dtheta, _p(self._scan_dev),
                 self.cfg.scan.beam_count, self.cfg.scan.fov, C.byref(self._noise),
                 C.byref(self._bp), _p(self.table), self.zdim, self.inv_res, self.cfg.seed, it,
-                est, stream))
-            self._est = PoseEstimate(est[0], est[1], est[2])
-            degenerate = st == RL_EDEGENERATE
+                _p(self.est_dev), stream))
         else:
-            degenerate = self._step_sharded(odo_dx, odo_dy, odo_dtheta, it, stream)
-        return MclStepResult(self._est, time.perf_counter() - t0, degenerate)
-
-    def _step_sharded(self, dx, dy, dth, it, stream) -> bool:
-        return sharded_step(self, self.stages or CudaStages(self, stream), dx, dy, dth, it)
+            sharded_step(self, self.stages or CudaStages(self, stream), odo_dx, odo_dy,
+                         odo_dtheta, it)
+        if cuda:
+            host = torch.empty(4, dtype=torch.float64, pin_memory=True)
+            host.copy_(self.est_dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.dev))
+            r = MclStepResult(host, ev, time.perf_counter() - t0)
+        else:
+            r = MclStepResult(self.est_dev.clone(), None, time.perf_counter() - t0)
+        self._last = r
+        return r
 
 
 class CudaStages:
-    """The per-shard stages of a sharded step, on this rank's GPU."""
+    """The per-shard stages of a sharded step on this rank's GPU, all on one
+    stream with no host synchronisation."""
 
     def __init__(self, m: "Mcl", stream):
         self.m, self.stream = m, stream
 
-    def motion(self, dx, dy, dth, it):
+    def sensor(self, dx, dy, dth, it):
+        """motion_update fused with the shard's log-weights and their max."""
         m = self.m
-        check(lib().rl_motion_update(_p(m.x), _p(m.y), _p(m.theta), m.n_local, m.offset, dx, dy,
-                                     dth, C.byref(m._noise), m.cfg.seed, it, self.stream))
-
-    def logw(self):
-        m = self.m
-        check(lib().rl_sensor_logw(m.cddt.handle, _p(m.x), _p(m.y), _p(m.theta), m.n_local,
-                                   _p(m._scan_dev), m.cfg.scan.beam_count, m.cfg.scan.fov,
-                                   C.byref(m._bp), _p(m.table), m.zdim, m.inv_res, _p(m.logw),
-                                   self.stream))
-        check(lib().rl_pf_max(_p(m.logw), m.n_local, _p(m.gmax), self.stream))
+        check(lib().rl_pf_shard_sensor(
+            m.cddt.handle, _p(m.x), _p(m.y), _p(m.theta), m.n_local, m.offset, dx, dy, dth,
+            C.byref(m._noise), m.cfg.seed, it, _p(m._scan_dev), m.cfg.scan.beam_count,
+            m.cfg.scan.fov, C.byref(m._bp), _p(m.table), m.zdim, m.inv_res, _p(m.logw),
+            _p(m.gmax), self.stream))
 
     def weights(self):
         m = self.m
@@ -205,47 +250,53 @@ class CudaStages:
         check(lib().rl_pf_normalize(_p(m.weight), m.n_local, _p(m.moments),
                                     m.cfg.particle_count, _p(m.flag), self.stream))
 
-    def resample(self, allp, it):
+    def estimate(self):
         m = self.m
-        check(lib().rl_resample_low_variance(
-            _p(allp[0]), _p(allp[1]), _p(allp[2]), _p(allp[3]), m.cfg.particle_count, m.offset,
-            m.n_local, _p(m.x), _p(m.y), _p(m.theta), _p(m.weight), m.cfg.seed, it, self.stream))
+        check(lib().rl_pf_estimate(_p(m.moments), _p(m.flag), m.cfg.particle_count,
+                                   _p(m.est_dev), self.stream))
+
+    def resample(self, it):
+        m = self.m
+        check(lib().rl_resample_gathered(
+            _p(m.gathered), m.n_local, m.world, m.offset, m.n_local, _p(m.x), _p(m.y),
+            _p(m.theta), _p(m.weight), m.cfg.seed, it, self.stream))
 
 
-def sharded_step(m: "Mcl", stages, dx, dy, dth, it) -> bool:
+def sharded_step(m: "Mcl", stages, dx, dy, dth, it) -> None:
     """One Mcl::step over particle shards: local stages with the two exchanges
-    of SURVEY.md §8e between them. `stages` supplies the local work (CUDA in
-    production; tests substitute a host implementation to check this
-    orchestration under a gloo group)."""
+    of SURVEY.md §8e between them, everything stream-ordered (no host
+    synchronisation; the estimate lands in m.est_dev). `stages` supplies the
+    local work (CUDA in production; tests substitute a host implementation to
+    check this orchestration under a gloo group)."""
     import torch
     import torch.distributed as dist
-    n = m.cfg.particle_count
-    stages.motion(dx, dy, dth, it)
-    stages.logw()  # logw and the local max
+    stages.sensor(dx, dy, dth, it)  # motion, log-weights and the local max
     dist.all_reduce(m.gmax, op=dist.ReduceOp.MAX, group=m.group)  # exchange 1a: max log-weight
     stages.weights()  # exp(logw - max) and pose moments
     dist.all_reduce(m.moments, op=dist.ReduceOp.SUM, group=m.group)  # exchange 1b: weight sum
     stages.normalize()
-    both = torch.cat([m.moments, m.flag.to(torch.float64)]).cpu().numpy()  # one read-back
-    mom, degenerate = both[:10], bool(both[10])
-    m._est = _estimate_from_moments(mom, n, degenerate)
-    # exchange 2: resampling gather; every rank resamples its own output slots
-    mine = torch.stack([m.x, m.y, m.theta, m.weight])
-    # rank-concatenated layout (world*4, n_local): accepted by NCCL and gloo
-    flat = torch.empty((m.world * 4, m.n_local), dtype=torch.float64, device=m.x.device)
-    if flat.device.type == "cuda":
-        dist.all_gather_into_tensor(flat, mine, group=m.group)
+    stages.estimate()
+    # exchange 2: resampling gather of the [4, n_local] blocks, rank-concatenated
+    # ([world * 4, n_local]); every rank resamples its own output slots from it
+    if m.gathered.device.type == "cuda" and dist.get_backend(m.group) == "nccl":
+        dist.all_gather_into_tensor(m.gathered, m.pblock, group=m.group)
+    elif m.gathered.device.type == "cuda":
+        # gloo (functional checks of this orchestration only): no CUDA all-gather,
+        # so the blocks go through host memory
+        host = torch.empty((m.world * 4, m.n_local), dtype=torch.float64)
+        dist.all_gather(list(host.view(m.world, 4, m.n_local).unbind(0)), m.pblock.cpu(),
+                        group=m.group)
+        m.gathered.copy_(host)
     else:
-        dist.all_gather(list(flat.view(m.world, 4, m.n_local).unbind(0)), mine, group=m.group)
-    full = flat.view(m.world, 4, m.n_local)
-    allp = full.permute(1, 0, 2).reshape(4, n).contiguous()
-    stages.resample(allp, it)
-    return degenerate
+        dist.all_gather(list(m.gathered.view(m.world, 4, m.n_local).unbind(0)), m.pblock,
+                        group=m.group)
+    stages.resample(it)
 
 
 def _estimate_from_moments(m, n, degenerate) -> PoseEstimate:
     """Mcl::estimate (mcl.cpp:176-187) from the weight moments
-    {sum e, sum e x, sum e y, sum e cos, sum e sin, n, sum x, sum y, sum cos, sum sin}."""
+    {sum e, sum e x, sum e y, sum e cos, sum e sin, n, sum x, sum y, sum cos, sum sin}
+    (host form, used by host-side stages; the GPU computes the same in rl_pf_estimate)."""
     if degenerate:
         sx, sy, sc, ss, sw = m[6] / n, m[7] / n, m[8] / n, m[9] / n, m[5] / n
     else:

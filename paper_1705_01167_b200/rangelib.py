@@ -143,6 +143,27 @@ def _cur_stream(t):
     return torch_stream(t.device)
 
 
+def _check_tensors(device: int, n: int, **arrays) -> None:
+    """Every array a batched entry point hands to the C ABI as a raw pointer:
+    a contiguous torch CUDA tensor on the structure's device with the dtype the
+    entry point expects and exactly n elements (None = optional and absent).
+    Raises ValueError instead of letting a kernel read or write out of bounds."""
+    import torch
+    for name, (t, dtype) in arrays.items():
+        if t is None:
+            continue
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{name}: expected a torch CUDA tensor, got {type(t).__name__}")
+        if t.device.type != "cuda" or t.device.index != device:
+            raise ValueError(f"{name}: tensor on {t.device}, structure on cuda:{device}")
+        if t.dtype != dtype:
+            raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name}: tensor must be contiguous")
+        if t.numel() != n:
+            raise ValueError(f"{name}: {t.numel()} elements, expected {n}")
+
+
 @dataclass
 class SliceProjection:
     """cddt.hpp:22-33 (read-only view)."""
@@ -309,17 +330,29 @@ class Cddt:
         """Batched casts. torch CUDA f32 tensors -> async on the current stream
         (or `stream`); numpy f32 arrays -> pipelined host path, returns numpy."""
         if isinstance(x, np.ndarray):
-            x, y, theta = (np.ascontiguousarray(a, dtype=np.float32) for a in (x, y, theta))
+            x, y, theta = (np.ascontiguousarray(a, dtype=np.float32).reshape(-1)
+                           for a in (x, y, theta))
+            if not (x.size == y.size == theta.size):
+                raise ValueError("x, y and theta must have the same length")
+            if hit is not None:
+                raise ValueError("hit cells are returned by the device path only")
             res = np.empty_like(x) if out is None else out
+            if not (isinstance(res, np.ndarray) and res.dtype == np.float32
+                    and res.flags.c_contiguous and res.flags.writeable and res.size == x.size):
+                raise ValueError("out must be a writable contiguous float32 array of len(x)")
             check(lib().rl_cddt_cast_batch_host(self._h, x.ctypes.data, y.ctypes.data,
                                                 theta.ctypes.data, res.ctypes.data, x.size))
             return res
         import torch
         if out is None:
             out = torch.empty_like(x)
+        n = x.numel()
+        f32 = torch.float32
+        _check_tensors(self._info.device, n, x=(x, f32), y=(y, f32), theta=(theta, f32),
+                       out=(out, f32), hit=(hit, torch.int32))
         s = stream if stream is not None else _cur_stream(x)
         check(lib().rl_cddt_cast_batch(self._h, _ptr(x), _ptr(y), _ptr(theta), _ptr(out),
-                                       _ptr(hit), x.numel(), s))
+                                       _ptr(hit), n, s))
         return out
 
     def cast_batch_f64(self, x, y, theta, out=None, hit=None, res_row=None, res_idx=None,
@@ -327,18 +360,25 @@ class Cddt:
         import torch
         if out is None:
             out = torch.empty_like(x)
+        n, f64 = x.numel(), torch.float64
+        _check_tensors(self._info.device, n, x=(x, f64), y=(y, f64), theta=(theta, f64),
+                       out=(out, f64), hit=(hit, torch.int32), res_row=(res_row, torch.int64),
+                       res_idx=(res_idx, torch.int32))
         s = stream if stream is not None else _cur_stream(x)
         check(lib().rl_cddt_cast_batch_f64(self._h, _ptr(x), _ptr(y), _ptr(theta), _ptr(out),
-                                           _ptr(hit), _ptr(res_row), _ptr(res_idx), x.numel(), s))
+                                           _ptr(hit), _ptr(res_row), _ptr(res_idx), n, s))
         return out
 
     def directional_batch(self, x, y, a, out=None, stream=None):
         import torch
         if out is None:
             out = torch.empty_like(x)
+        n, f64 = x.numel(), torch.float64
+        _check_tensors(self._info.device, n, x=(x, f64), y=(y, f64), a=(a, torch.int32),
+                       out=(out, f64))
         s = stream if stream is not None else _cur_stream(x)
         check(lib().rl_cddt_directional_batch(self._h, _ptr(x), _ptr(y), _ptr(a), _ptr(out),
-                                              x.numel(), s))
+                                              n, s))
         return out
 
     def exact_cast_batch(self, x, y, theta=None, cos_t=None, sin_t=None, out=None, stream=None):
@@ -346,9 +386,16 @@ class Cddt:
         import torch
         if out is None:
             out = torch.empty_like(x)
+        n, f64 = x.numel(), torch.float64
+        if (cos_t is None) != (sin_t is None):
+            raise ValueError("cos_t and sin_t are given together or not at all")
+        if theta is None and cos_t is None:
+            raise ValueError("exact casts need theta or cos_t/sin_t")
+        _check_tensors(self._info.device, n, x=(x, f64), y=(y, f64), theta=(theta, f64),
+                       cos_t=(cos_t, f64), sin_t=(sin_t, f64), out=(out, f64))
         s = stream if stream is not None else _cur_stream(x)
         check(lib().rl_exact_cast_batch(self._h, _ptr(x), _ptr(y), _ptr(theta), _ptr(cos_t),
-                                        _ptr(sin_t), _ptr(out), x.numel(), s))
+                                        _ptr(sin_t), _ptr(out), n, s))
         return out
 
     def simulate_scans(self, x, y, theta, spec: "ScanSpec", max_range: float,
@@ -361,6 +408,10 @@ class Cddt:
         n = x.numel()
         if out is None:
             out = torch.empty((n, spec.beam_count), dtype=torch.float64, device=x.device)
+        f64, nb = torch.float64, spec.beam_count
+        _check_tensors(self._info.device, n, x=(x, f64), y=(y, f64), theta=(theta, f64))
+        _check_tensors(self._info.device, n * nb, cos_t=(cos_t, f64), sin_t=(sin_t, f64),
+                       out=(out, f64))
         s = stream if stream is not None else _cur_stream(x)
         check(lib().rl_simulate_scans(self._h, _ptr(x), _ptr(y), _ptr(theta), n, spec.beam_count,
                                       spec.fov, float(max_range), float(noise_sigma), seed,
@@ -542,13 +593,16 @@ def beam_table(p: BeamModelParams, zdim: int, inv_res: float = 1.0) -> np.ndarra
 
 
 def sensor_update(particles, method, scan, spec: ScanSpec, beam: BeamModelParams, table=None,
-                  inv_res: float = 1.0, logw=None) -> bool:
+                  inv_res: float = 1.0, logw=None, degenerate=None):
     """sensor_update (mcl.cpp:58-120) on the GPU.
 
     particles: dict-like with torch CUDA f64 tensors 'x', 'y', 'theta', 'weight'
     (weights are overwritten, as the reference overwrites Particle::weight).
     scan: torch CUDA f64 [beam_count]. table: optional torch CUDA f32 [zdim, zdim].
-    Returns False when the weights were degenerate and reset to uniform.
+    Returns False when the weights were degenerate and reset to uniform (this
+    waits for the device). With `degenerate` (a torch CUDA int32 [1] tensor) the
+    update is only queued on the current stream (rl_sensor_update_async): the
+    flag lands in that tensor (1 = degenerate) and the call returns None.
     """
     cddt = method.cddt if isinstance(method, CddtMethod) else method
     if scan.numel() != spec.beam_count:
@@ -558,7 +612,23 @@ def sensor_update(particles, method, scan, spec: ScanSpec, beam: BeamModelParams
         bp = BeamModelParams(**{**bp.__dict__, "z_max": cddt.max_range()})
     x, y, t, w = particles["x"], particles["y"], particles["theta"], particles["weight"]
     zdim = 0 if table is None else int(table.shape[0])
+    import torch
+    dev, n, f64 = cddt.info().device, x.numel(), torch.float64
+    _check_tensors(dev, n, x=(x, f64), y=(y, f64), theta=(t, f64), weight=(w, f64),
+                   logw=(logw, f64))
+    _check_tensors(dev, spec.beam_count, scan=(scan, f64))
+    if table is not None:
+        if table.dim() != 2 or table.shape[0] != table.shape[1]:
+            raise ValueError("table must be square [zdim, zdim]")
+        _check_tensors(dev, zdim * zdim, table=(table, torch.float32))
+    if degenerate is not None:
+        _check_tensors(dev, 1, degenerate=(degenerate, torch.int32))
+        check(lib().rl_sensor_update_async(
+            cddt.handle, _ptr(x), _ptr(y), _ptr(t), n, _ptr(scan), spec.beam_count, spec.fov,
+            C.byref(bp.c()), _ptr(table), zdim, inv_res, _ptr(logw), _ptr(w), _ptr(degenerate),
+            _cur_stream(x)))
+        return None
     st = check(lib().rl_sensor_update(
-        cddt.handle, _ptr(x), _ptr(y), _ptr(t), x.numel(), _ptr(scan), spec.beam_count, spec.fov,
+        cddt.handle, _ptr(x), _ptr(y), _ptr(t), n, _ptr(scan), spec.beam_count, spec.fov,
         C.byref(bp.c()), _ptr(table), zdim, inv_res, _ptr(logw), _ptr(w), _cur_stream(x)))
     return st != _lib.RL_EDEGENERATE

@@ -1,10 +1,17 @@
-/* Checks the walker's division shortcut (cddt_device.cuh div_rn):
- *   q0 = RN(a * r), e = fma(-d, q0, a), q = fma(e, r, q0), r = RN(1/d)
+/* Checks the walker's division (cddt_device.cuh div_rn):
+ *   q0 = RN(a * r), q1 = fma(fma(-d, q0, a), r, q0), q = fma(fma(-d, q1, a), r, q1),
+ *   r = RN(1/d)
  * against IEEE a / d, bit for bit, over the operands the walker produces:
  * d = every non-axis direction cosine/sine of the theta_disc lattices
  * (direction_components, proj/src/cddt.cpp:30-42) and a = cell boundary -
- * origin, origin a float-widened coordinate or a cell centre.
- * Usage: fast_div_check <samples per direction>  -> prints "checked N mismatches M" */
+ * origin, the origin a float-widened coordinate (batched casts), an arbitrary
+ * f64 coordinate (sensor-model and particle-filter poses), a cell centre
+ * (prune) or a float one ulp off a lattice line. The two-step form is correct
+ * by Markstein's theorem (see div_rn); this is the empirical cross-check. It
+ * also counts how often the ONE-step form RN(q0 + RN(a - d q0) r) would have
+ * differed ("one_step_mismatches", informational: it is not used).
+ * Usage: fast_div_check <samples per direction>
+ *   -> prints "checked N mismatches M one_step_mismatches M1" */
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -21,18 +28,19 @@ static inline uint64_t nxt(void) {
 }
 static inline double u01(void) { return (double)(nxt() >> 11) * 0x1.0p-53; }
 
-static long checked = 0, bad = 0;
+static long checked = 0, bad = 0, bad1 = 0;
 static void check(double a, double d) {
   double r = 1.0 / d;
   double q0 = a * r;
-  double e = fma(-d, q0, a);
-  double q = fma(e, r, q0);
+  double q1 = fma(fma(-d, q0, a), r, q0);
+  double q = fma(fma(-d, q1, a), r, q1);
   double ref = a / d;
   checked++;
   if (q != ref || signbit(q) != signbit(ref)) {
     if (bad < 10) printf("mismatch a=%a d=%a q=%a ref=%a\n", a, d, q, ref);
     bad++;
   }
+  if (q1 != ref) bad1++;
 }
 
 int main(int argc, char **argv) {
@@ -54,6 +62,9 @@ int main(int argc, char **argv) {
           double o = (double)of;
           check((double)c + 1.0 - o, d);
           check((double)c - o, d);
+          double od = u01() * 8192.0; /* f64 origins: particle poses */
+          check((double)c + 1.0 - od, d);
+          check((double)c - od, d);
           double oc = (double)(int)(u01() * 8192.0) + 0.5; /* prune: cell centres */
           check((double)c + 1.0 - oc, d);
           check((double)c - oc, d);
@@ -77,6 +88,6 @@ int main(int argc, char **argv) {
     }
     for (int i = 0; i <= K; i++) check((double)i * TWO_PI / (double)K * (double)K, TWO_PI);
   }
-  printf("checked %ld mismatches %ld\n", checked, bad);
+  printf("checked %ld mismatches %ld one_step_mismatches %ld\n", checked, bad, bad1);
   return bad != 0;
 }

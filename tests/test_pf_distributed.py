@@ -36,6 +36,10 @@ class HostStages:
     def _np(self, t):
         return t.numpy()
 
+    def sensor(self, dx, dy, dth, it):
+        self.motion(dx, dy, dth, it)
+        self.logw()
+
     def motion(self, dx, dy, dth, it):
         import ctypes as C
         m = self.m
@@ -73,10 +77,18 @@ class HostStages:
             m.weight.div_(s)
         m.flag.fill_(1 if bad else 0)
 
-    def resample(self, allp, it):
+    def estimate(self):
+        from paper_1705_01167_b200 import mcl
+        m = self.m
+        e = mcl._estimate_from_moments(m.moments.numpy(), m.cfg.particle_count, bool(m.flag[0]))
+        m.est_dev.copy_(torch.tensor([e.x, e.y, e.theta, float(m.flag[0])], dtype=torch.float64))
+
+    def resample(self, it):
         import ctypes as C
         m = self.m
         n = m.cfg.particle_count
+        # the rank-concatenated all-gather block [world * 4, n_local] -> rows x, y, theta, w
+        allp = m.gathered.view(m.world, 4, m.n_local).permute(1, 0, 2).reshape(4, n)
         a = [np.ascontiguousarray(allp[k].numpy()) for k in range(4)]
         out = [np.empty(n) for _ in range(4)]
         self.L.orc_resample.argtypes = [C.c_void_p] * 4 + [C.c_long] + [C.c_void_p] * 5 + \
