@@ -624,6 +624,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->d_rbase.release();
     c->d_scalar.release();
     c->ws.release();
+    c->sensor_ctl.release();
     c->upd_ws.release();
     c->zp_spare.release();
     c->off_spare.release();

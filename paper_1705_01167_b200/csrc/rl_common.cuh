@@ -124,6 +124,8 @@ struct rl_cddt {
   rl::DevBuf<uint32_t> d_rbase;  // S slice row bases (batch phase 1)
   rl::DevBuf<double> d_scalar;      // scratch for single-query calls
   rl::DevBuf<uint8_t> ws;           // reusable workspace (sensor model reductions)
+  rl::DevBuf<uint8_t> sensor_ctl;   // sensor_update's fused normalisation: {max key, ticket, flag}
+  bool sensor_ctl_clean = false;    // its key and ticket are zero (every completed launch leaves them so)
   std::mutex mu;                    // serialises users of d_scalar / ws / pf_* / the handle stream
   rl::DevBuf<uint8_t> pf_ctl;       // fused PF step: {max key, ticket} | moments (zeroed when dirty)
   bool pf_ctl_clean = false;        // the max key is 0 (every completed step leaves it so)

@@ -39,7 +39,9 @@ namespace cg = cooperative_groups;
 int sensor_logw_launch(rl_cddt* c, double* px, double* py, double* pt, size_t n,
                        const double* scan, int nb, double fov, const rl_beam_params_t* params,
                        const float* table, int zdim, double inv_res, double* logw,
-                       const MotionArgs* mot, unsigned long long* gmax_key, cudaStream_t st);
+                       const MotionArgs* mot, unsigned long long* gmax_key, cudaStream_t st,
+                       double* tail_w = nullptr, int32_t* tail_flag = nullptr,
+                       unsigned* tail_ticket = nullptr);
 
 __global__ void k_motion(double* __restrict__ x, double* __restrict__ y, double* __restrict__ t,
                          size_t n, MotionArgs m) {
