@@ -1,7 +1,11 @@
 """Summarise an `ncu --set full` capture into the text committed under
-profiles/: headline metrics, warp-stall breakdown and the hottest SASS lines.
+profiles/: headline metrics per launch, then the warp-stall breakdown and the
+hottest SASS lines. The source page of a report aggregates every launch in it,
+so the stall/SASS sections are printed only for single-launch reports (capture
+one kernel per report: `-k regex:<name> -s <skip> -c 1`); SASS lines are
+listed once per address.
 
-    python profiles/summarize_ncu.py gpurun_out/prof_cast.ncu-rep [queries] > profiles/rNN/....txt
+    python profiles/summarize_ncu.py gpurun_out/prof_cast.ncu-rep [units] > profiles/rNN/....txt
 """
 import csv
 import io
@@ -50,6 +54,10 @@ def main():
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             tot = tob(*got["dram__bytes_read.sum"]) + tob(*got["dram__bytes_write.sum"])
             print(f"  dram bytes per unit ({units:.0f} units): {tot / units:.2f}")
+    if len(vals) != 1:
+        print(f"== {len(vals)} launches in this report: stall and SASS sections skipped "
+              "(they would aggregate all launches)")
+        return
     sass = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source",
                                            "sass"))))
     if len(sass) < 3:
@@ -68,7 +76,13 @@ def main():
     for s, v in sorted(((s, sum(f(r, s) for r in data)) for s in stalls), key=lambda x: -x[1])[:10]:
         print(f"  {s:28s} {100 * v / tot:5.1f}")
     print("== hottest SASS (samples, warp-instructions executed, avg active threads)")
-    for r in sorted(data, key=lambda r: -f(r, "Warp Stall Sampling (All Samples)"))[:25]:
+    seen, uniq = set(), []
+    for r in data:
+        key = r[ix["Address"]] if "Address" in ix else r[ix["Source"]]
+        if key not in seen:
+            seen.add(key)
+            uniq.append(r)
+    for r in sorted(uniq, key=lambda r: -f(r, "Warp Stall Sampling (All Samples)"))[:25]:
         print(f"  {r[ix['Source']][:64]:64s} {int(f(r, 'Warp Stall Sampling (All Samples)')):8d} "
               f"{int(f(r, 'Instructions Executed')):11d} {f(r, 'Avg. Threads Executed'):5.1f}")
 

@@ -394,6 +394,32 @@ def test_full_size_structure_and_casts_vs_reference_hashes(rl, synth, name):
     assert _sha(host(o32)) == want["casts_f32_sha"]
 
 
+def test_cfg3_split_pipeline_16M_vs_reference_hashes(rl, synth):
+    """The headline path itself: 16M config-3 queries through the split cast
+    pipeline (two pipelines of phase 1 / near field / window passes, batches >=
+    8M), f32 ranges sha-equal to float(the reference's f64 casts) on the
+    reference-built PCDDT; the GPU-built PCDDT serialises to the reference's
+    snapshot bytes (sha in oracle/cfg3_pcddt.sha256); f64 ranges (single-kernel
+    path) sha-equal to the reference's."""
+    import torch
+    from pathlib import Path
+    want = LARGE.get("cfg3_pcddt_split16M")
+    if want is None:
+        pytest.skip("tests/golden/large.json has no cfg3_pcddt_split16M")
+    g = synth.polygon_map()
+    c = make_gpu(rl, g, 200, 1000.0, prune=True)
+    ref_sha = (Path(__file__).resolve().parents[1] / "oracle" / "cfg3_pcddt.sha256").read_text()
+    assert _sha(np.frombuffer(rl.serialize_cddt(c), np.uint8)) == ref_sha.split()[0]
+    qx, qy, qt = synth.free_queries(g, want["queries"], seed=want["query_seed"])
+    o32 = c.cast_batch(dev(qx), dev(qy), dev(qt))
+    torch.cuda.synchronize()
+    assert _sha(host(o32)) == want["casts_f32_sha"]
+    out = c.cast_batch_f64(*(dev(a.astype(np.float64)) for a in (qx, qy, qt)))
+    assert _sha(host(out)) == want["casts_sha"]
+    # the host-pointer pipeline (chunked H2D / cast / D2H) on the same stream
+    assert _sha(c.cast_batch(qx, qy, qt)) == want["casts_f32_sha"]
+
+
 def test_full_size_edit_rounds_vs_reference_hashes(rl, synth):
     """Config 5: 2000x2000 maze, theta_disc 108, rounds of 50 random 3x3
     insert/remove blocks; zero points bit-exact with the reference after every
