@@ -171,6 +171,13 @@ int rl_cddt_sync(rl_cddt *c);
 int rl_diag_gather(const void *buf, size_t bytes, size_t loads, void *stream, double *ms,
                    uint64_t *issued);
 
+/* Diagnostic (no reference counterpart): device bounds assertions of a
+ * checked build (compiled with -DRL_CHECKED; compute-sanitizer stand-in).
+ * *failures = violated assertions on `device` so far, *first_code = the site
+ * of the first one (cddt_device.cuh RL_DCHECK codes). A regular build reports
+ * 0 failures and first_code 0xFFFFFFFF. Synchronises the device. */
+int rl_debug_checks(int32_t device, uint64_t *failures, uint32_t *first_code);
+
 /* ---- beam sensor model and particle filter (proj/src/mcl.cpp) ---- */
 
 /* BeamModelParams (proj/include/rangelib/mcl.hpp:32-40). */

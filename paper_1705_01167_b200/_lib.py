@@ -73,6 +73,7 @@ _SIG = {
     "rl_cddt_sync": (C.c_int, [_P]),
     "rl_diag_gather": (C.c_int, [_P, C.c_size_t, C.c_size_t, _P, C.POINTER(C.c_double),
                                  C.POINTER(C.c_uint64)]),
+    "rl_debug_checks": (C.c_int, [C.c_int32, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     "rl_beam_likelihood": (C.c_double, [C.POINTER(rl_beam_params_t), C.c_double, C.c_double]),
     "rl_beam_table": (C.c_int, [C.POINTER(rl_beam_params_t), C.c_int32, C.c_double, _P]),
     "rl_sensor_update": (C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int32, C.c_double,

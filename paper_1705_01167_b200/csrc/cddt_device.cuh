@@ -50,7 +50,27 @@ struct CddtView {
   const uint32_t* __restrict__ rbase;     // S: slice row bases (4 B each: a few lines in all)
   int w, h, K, S;
   double max_range;
+  // checked builds (-DRL_CHECKED): bounds of the arrays above and the
+  // violation counter {count, first code} the device assertions bump
+  unsigned long long* chk;
+  uint32_t n_rows, n_zp;
 };
+
+// Device bounds assertions of the checked build (RL_CHECKED; compute-sanitizer
+// is unavailable on the GPU pool): a failed check bumps c.chk[0] and records
+// its site code in c.chk[1]; rl_debug_checks() reads them back. Compiled out
+// otherwise.
+#ifdef RL_CHECKED
+static __device__ __noinline__ void rl_check_fail(unsigned long long* chk, unsigned code) {
+  if (chk && atomicAdd(chk, 1ull) == 0ull) chk[1] = code;
+}
+#define RL_DCHECK(view, cond, code)                          \
+  do {                                                       \
+    if (!(cond)) ::rl::rl_check_fail((view).chk, (code));    \
+  } while (0)
+#else
+#define RL_DCHECK(view, cond, code) ((void)0)
+#endif
 
 __host__ __device__ __forceinline__ double fmin_std(double a, double b) { return (b < a) ? b : a; }
 __host__ __device__ __forceinline__ double fmax_std(double a, double b) { return (a < b) ? b : a; }
@@ -107,6 +127,7 @@ __device__ __forceinline__ bool in_bounds(const CddtView& c, int x, int y) {
   return (unsigned)x < (unsigned)c.w && (unsigned)y < (unsigned)c.h;
 }
 __device__ __forceinline__ bool occupied(const CddtView& c, int x, int y) {
+  RL_DCHECK(c, unsigned(x) < unsigned(c.w) && unsigned(y) < unsigned(c.h), 1);
   return (__ldg(&c.rowbits[y * c.wpr + (x >> 5)].x) >> (x & 31)) & 1u;
 }
 
@@ -397,6 +418,7 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   if (row < 0) row = 0;
   if (row >= sp.bin_count) row = sp.bin_count - 1;
   q.g = sp.row_base + (uint32_t)row;
+  RL_DCHECK(c, s >= 0 && s < c.S && q.g < c.n_rows, 2);
   // requested together with the origin cell's bits: the two are independent
   // one 32-byte load (LDG.256) rather than two 16-byte ones: one L1 wavefront per lane
   const RowRecord rec = reinterpret_cast<const RowRecord*>(c.hints)[q.g];
@@ -404,6 +426,7 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   q.hint2 = rec.b;
   q.lo = __float_as_uint(q.hint.x);
   q.hi = q.lo + __float_as_uint(q.hint.y);
+  RL_DCHECK(c, q.lo <= q.hi && q.hi <= c.n_zp, 4);  // every zero-point read lies in [lo, hi)
   return q;
 }
 
@@ -442,11 +465,13 @@ __device__ __forceinline__ QueryRow query_row(const CddtView& c, double x, doubl
   if (row < 0) row = 0;
   if (row >= bin_count) row = bin_count - 1;
   q.g = __ldg(c.rbase + s) + uint32_t(row);
+  RL_DCHECK(c, a >= 0 && a < c.K && q.g < c.n_rows, 3);
   const RowRecord rec = reinterpret_cast<const RowRecord*>(c.hints)[q.g];
   q.hint = rec.a;
   q.hint2 = rec.b;
   q.lo = __float_as_uint(q.hint.x);
   q.hi = q.lo + __float_as_uint(q.hint.y);
+  RL_DCHECK(c, q.lo <= q.hi && q.hi <= c.n_zp, 4);  // every zero-point read lies in [lo, hi)
   return q;
 }
 
@@ -475,6 +500,7 @@ __device__ __forceinline__ double directional_cast(const CddtView& c, double x, 
   if (!in_bounds(c, cxi, cyi)) return c.max_range;  // cddt.cpp:209
   double2 d2;  // the direction's cos/sin; the walker's full entry is read when one is needed
   const QueryRow q = query_row(c, x, y, a, &d2);
+  RL_DCHECK(c, unsigned(cxi) < unsigned(c.w) && unsigned(cyi) < unsigned(c.h), 5);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {  // cddt.cpp:210
     o.hit = cyi * c.w + cxi;
@@ -549,6 +575,7 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
   }
   double2 dir;
   const QueryRow q = query_row(c, x, y, a, &dir);
+  RL_DCHECK(c, unsigned(cxi) < unsigned(c.w) && unsigned(cyi) < unsigned(c.h), 5);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {
     *result = 0.0;
@@ -619,6 +646,7 @@ __device__ __forceinline__ bool resume_windows(const CddtView& c, double x, doub
   const double xq = x * cs + y * sn;
   const float* __restrict__ v = c.zp + s.lo;
   const int n = (int)s.n, step = forward ? 1 : -1;
+  RL_DCHECK(c, uint64_t(s.lo) + s.n <= c.n_zp && a >= 0 && a < c.K, 6);
   Walker<true> wk;
   int idx = s.idx, windows = 0;
   if (FRESH) {

@@ -109,6 +109,25 @@ void handle_closed(int dev) {
   cudaMemPoolTrimTo(ps.pool, 0);
 }
 
+// Checked builds: one zeroed {count, first code} pair per device, allocated
+// on first use; every view carries it to the device assertions (RL_DCHECK).
+unsigned long long* check_counter(int dev) {
+#ifdef RL_CHECKED
+  static unsigned long long* ctr[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  unsigned long long*& p = ctr[dev & 63];
+  if (!p) {
+    DeviceGuard guard(dev);
+    if (cudaMalloc(&p, 16) != cudaSuccess || cudaMemset(p, 0, 16) != cudaSuccess) p = nullptr;
+  }
+  return p;
+#else
+  (void)dev;
+  return nullptr;
+#endif
+}
+
 int finish(const rl_cddt* c, void* s) {
   RL_CK(cudaGetLastError());
   if (!s) RL_CK(cudaStreamSynchronize(c->stream));
@@ -557,6 +576,27 @@ using namespace rl;
 extern "C" {
 
 const char* rl_last_error(void) { return g_err.c_str(); }
+
+int rl_debug_checks(int32_t device, uint64_t* failures, uint32_t* first_code) {
+  if (!failures || !first_code) return RL_EINVAL;
+#ifdef RL_CHECKED
+  unsigned long long* p = check_counter(device);
+  unsigned long long h[2] = {0, 0};
+  if (p) {
+    DeviceGuard guard(device);
+    RL_CK(cudaDeviceSynchronize());
+    RL_CK(cudaMemcpy(h, p, sizeof h, cudaMemcpyDeviceToHost));
+  }
+  *failures = h[0];
+  *first_code = uint32_t(h[1]);
+  return RL_OK;
+#else
+  (void)device;
+  *failures = 0;
+  *first_code = 0xFFFFFFFFu;  // not a checked build
+  return RL_OK;
+#endif
+}
 
 int rl_cddt_create(const uint8_t* grid, int32_t width, int32_t height, double resolution,
                    int32_t theta_disc, double max_range, int32_t prune, int32_t device,

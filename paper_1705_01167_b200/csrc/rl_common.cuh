@@ -93,6 +93,11 @@ struct DeviceGuard {
 
 }  // namespace rl
 
+namespace rl {
+// checked builds: the device violation counter of `dev` (nullptr otherwise)
+unsigned long long* check_counter(int dev);
+}  // namespace rl
+
 // The opaque handle (include/rl_cddt.h). Owns the device copy of the flags
 // and the CSR structure on one device, plus host mirrors of the grid and
 // membership (small: w*h bytes) that drive incremental edits.
@@ -152,6 +157,9 @@ struct rl_cddt {
     v.K = K;
     v.S = S;
     v.max_range = max_range;
+    v.chk = rl::check_counter(dev);
+    v.n_rows = uint32_t(rows);
+    v.n_zp = uint32_t(zero_points);
     return v;
   }
 };

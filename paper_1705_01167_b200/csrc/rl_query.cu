@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
       const unsigned below = (1u << lane) - 1;
       const size_t slot = win ? base_s[0] + cnt_s[0][wid] + __popc(bw & below)
                               : n - 1 - (base_s[1] + cnt_s[1][wid] + __popc(bn & below));
+      // window records grow up, near-field records down: together at most n
+      RL_DCHECK(c, slot < n && base_s[0] + base_s[1] <= n, 10);
       const float4* src = reinterpret_cast<const float4*>(&rec);
       st256_cs(q + slot, src[0], src[1]);
     }
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
     __syncthreads();
     if (defer) {
       const unsigned slot = base_s + cnt_s[wid] + __popc(bal & ((1u << lane) - 1));
+      RL_DCHECK(c, qi < 0x80000000u && k < in_cap, 11);
       if (slot < out_cap) {  // ContRecord layout, as three 16-byte stores
         float4* dst = reinterpret_cast<float4*>(oq + slot);
         __stcs(dst, make_float4(fx, fy, ft, __uint_as_float(qi)));
@@ -282,6 +285,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
     WinState s{};
     int a = 0;
     if (k < m) {
+      RL_DCHECK(c, k < n, 12);
       w0 = __ldcs(reinterpret_cast<const float4*>(q + (n - 1 - k)));  // x, y, theta, index
       a = direction_index(normalize_angle_2pi(double(w0.z)), c.K);
       double res;

@@ -358,6 +358,7 @@ __device__ __forceinline__ void slice_casts(const CddtView& c, double x, double 
     return;
   }
   const QueryRow q = query_row(c, x, y, s);
+  RL_DCHECK(c, unsigned(cxi) < unsigned(c.w) && unsigned(cyi) < unsigned(c.h), 5);
   const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
   if ((w0.x >> (cxi & 31)) & 1u) {  // cddt.cpp:210
     *rf = *rb = 0.0;
@@ -450,6 +451,7 @@ __global__ void __launch_bounds__(256, kSensorParticlesPerCta < 16 ? RL_SENSOR_M
     if (p0 + pl >= n) continue;
     const double x = pose[0][pl], y = pose[1][pl], t = pose[2][pl];
     const int b1 = jobs.b1[j], b2 = jobs.b2[j];
+    RL_DCHECK(c, j < jobs.n && b1 >= 0 && b1 < nb && b2 < nb && pl < kSensorParticlesPerCta, 20);
     const int a1 = direction_index(normalize_angle_2pi(t + boff[b1]), c.K);
     const int a2 = b2 < 0 ? -1 : direction_index(normalize_angle_2pi(t + boff[b2]), c.K);
     // one slice visit for an exactly opposite pair, else one per beam

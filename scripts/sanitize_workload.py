@@ -1,11 +1,11 @@
-"""Small workload touching every kernel family of librl_cddt.so, for
-compute-sanitizer (memcheck / racecheck / synccheck). Run against the variant
-library built with -DRL_DEFER_MIN_LOG2=12 so the split cast pipeline (phase 1,
-near-field kernel, window passes, continuation queues) runs on small batches;
+"""Small workload touching every kernel family of librl_cddt.so, run against
+the checked library (-DRL_CHECKED: device bounds assertions, read back through
+rl_debug_checks; compute-sanitizer is closed on the GPU pool) built with
+-DRL_DEFER_MIN_LOG2=12 so the split cast pipeline (phase 1, near-field kernel,
+window passes, continuation queues) runs on small batches;
 RL_CDDT_CONT_CAP=1 additionally forces the queue-full path.
 
-    RL_CDDT_LIB=paper_1705_01167_b200/librl_cddt_san.so \\
-      compute-sanitizer --tool memcheck python scripts/sanitize_workload.py
+    RL_CDDT_LIB=paper_1705_01167_b200/librl_cddt_checked.so python scripts/sanitize_workload.py
 """
 import ctypes as C
 import math
@@ -94,5 +94,14 @@ L.rl_resample_gathered(gat.data_ptr(), 1000, 3, 1000, 1000, *(out[k].data_ptr() 
 L.rl_pf_shard_sensor(c.handle, f.x.data_ptr(), f.y.data_ptr(), f.theta.data_ptr(), n, 0, 1.0, 0.0,
                      0.0, C.byref(f._noise), 1, 0, scan.data_ptr(), 61, FOV, C.byref(f._bp),
                      table.data_ptr(), 151, 1.0, lw.data_ptr(), mx.data_ptr(), st)
+if "--negative" in sys.argv:  # control: an out-of-range direction must trip the assertions
+    bad = torch.full((4,), 24, dtype=torch.int32, device="cuda")  # theta_disc is 24
+    c.directional_batch(torch.full((4,), 10.5, dtype=torch.float64, device="cuda"),
+                        torch.full((4,), 20.5, dtype=torch.float64, device="cuda"), bad)
 torch.cuda.synchronize()
-print("sanitize workload done", math.isfinite(f.estimate().x))
+nf, code = C.c_uint64(), C.c_uint32()
+L.rl_debug_checks(0, C.byref(nf), C.byref(code))
+print("sanitize workload done", math.isfinite(f.estimate().x), "device check failures", nf.value,
+      "first site", code.value)
+assert code.value != 0xFFFFFFFF, "not a checked build"
+assert (nf.value > 0) if "--negative" in sys.argv else (nf.value == 0)

@@ -42,3 +42,22 @@ def rl():
 def synth():
     from paper_1705_01167_b200 import synth
     return synth
+
+
+@pytest.fixture(autouse=True)
+def _device_bounds_checks(request):
+    """With a checked library (built with -DRL_CHECKED and selected through
+    RL_CDDT_LIB; the compute-sanitizer stand-in), every GPU test ends with
+    zero failed device bounds assertions."""
+    yield
+    if "gpu" not in request.keywords or not os.environ.get("RL_CHECKED_SUITE"):
+        return
+    import ctypes as C
+
+    from paper_1705_01167_b200 import _lib
+    if _lib._lib is None:
+        return
+    n, code = C.c_uint64(), C.c_uint32()
+    assert _lib._lib.rl_debug_checks(0, C.byref(n), C.byref(code)) == 0
+    assert code.value != 0xFFFFFFFF, "RL_CHECKED_SUITE set but the library is not a checked build"
+    assert n.value == 0, f"{n.value} device bounds assertions failed (first: site {code.value})"
