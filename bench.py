@@ -616,6 +616,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE config-3 map and query stream)",
             "config": dict(workload_config(n), parallelism=f"query-sharded x{world}, structure replicated",
+                           dist_backend=(dist.get_backend() if world > 1 else None),
                            zero_points=int(info.zero_points), rows=int(info.rows),
                            device_bytes=int(info.device_bytes),
                            build_plus_prune_s=round(info.init_seconds, 3)),
@@ -629,6 +630,8 @@ def run_ours(args, rank, world, local_rank):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{peak_kind} hbm_gbs",
                          "algorithmic_bytes_per_query": bytes_per_query, "sectors_per_query": s_bar,
+                         "l2_sectors_per_query": (tr or {}).get("l2_sectors_per_query"),
+                         "traffic_source": (tr or {}).get("source"),
                          "sector_sample": ns,
                          "kernel": "batched cast = 2 pipelines (halves of the batch, two streams) of "
                                    "k_cast_defer_p1 + k_cast_near + 4 x k_walk_pass (window passes); "

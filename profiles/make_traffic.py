@@ -1,6 +1,8 @@
 """profiles/traffic.json from a committed ncu summary of one full config-3 step
 (summarize_ncu.py output over all the step's kernels, 100M queries):
-    python profiles/make_traffic.py profiles/r01/ncu_k_cast_defer_vNN.txt"""
+    python profiles/make_traffic.py profiles/r02/ncu_step_warm.txt
+(round 2 wrote the committed traffic.json from the warm capture, adding the
+cold-cache figures of profiles/r02/ncu_step_cold.txt by hand)"""
 import collections
 import json
 import re
