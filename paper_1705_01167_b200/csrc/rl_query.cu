@@ -539,16 +539,20 @@ using namespace rl;
 
 extern "C" {
 
+// One query (Cddt::cast / cast_pair): a one-thread kernel that writes its
+// answer straight into the handle's pinned host words (device-visible under
+// unified addressing), then one stream synchronisation — no copy operation.
+// The round trip is launch-latency bound (INTEGRATION.md "Per-ray calls");
+// batches go through the _batch entry points.
 static int single(rl_cddt* c, double x, double y, double theta, int pair, double* o0,
                   double* o1) {
   std::lock_guard<std::mutex> lock(c->mu);
   DeviceGuard guard(c->dev);
-  if (!c->d_scalar.p) RL_TRY(c->d_scalar.alloc(2));
-  k_single<<<1, 1, 0, c->stream>>>(c->view(), x, y, theta, pair, c->d_scalar.p);
+  uint32_t* hs = nullptr;
+  RL_TRY(host_small(c, &hs));
+  double* r = reinterpret_cast<double*>(hs);
+  k_single<<<1, 1, 0, c->stream>>>(c->view(), x, y, theta, pair, r);
   RL_CK(cudaGetLastError());
-  double r[2];
-  RL_CK(cudaMemcpyAsync(r, c->d_scalar.p, sizeof(double) * (pair ? 2 : 1), cudaMemcpyDeviceToHost,
-                        c->stream));
   RL_CK(cudaStreamSynchronize(c->stream));
   *o0 = r[0];
   if (pair) *o1 = r[1];
