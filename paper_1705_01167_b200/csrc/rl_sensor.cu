@@ -135,138 +135,6 @@ __device__ __forceinline__ void normalize_tail(const NormTail& nt,
 // MOTION: the CTA's particles first take their motion_update step (the fused
 // Mcl::step, mcl.cpp:189-193) and write the moved poses back. gmax_key (may be
 // null) receives the order-preserving atomic max of the log-weights.
-// ---- long casts: the candidate loop evaluated a warp at a time ----
-//
-// A ray grazing a wall meets one failing candidate per wall cell, so a few
-// casts run tens of verification windows while their warp and CTA wait: in a
-// sensor update that fits the GPU in one wave (config 2), those casts decide
-// the kernel time. Each candidate's verdict is a pure function of the
-// candidate: its landing probe, and the cells of its window [d - 0.7072,
-// d + 0.7072] (cddt.cpp:236-262). The reference's single walker covers each
-// window from max(its position, d - 0.7072); the cells between d - 0.7072 and
-// that position were already entered and found free by the earlier windows
-// or the near-field walk, so a fresh walker placed at d - 0.7072 reaches the
-// same verdict (hit, clean, or leaving the grid). The first non-clean verdict
-// in candidate order decides the cast exactly as the sequential loop does —
-// so 32 lanes can evaluate 32 consecutive candidates at once.
-//
-// Phase A (every thread, its own items) stops a cast after kLongCap windows
-// and queues it in shared memory {pose, direction, next candidate, ll slot};
-// phase B hands each queued cast to a whole warp (resume_coop).
-#ifndef RL_SENSOR_WCAP
-#define RL_SENSOR_WCAP 4  // windows a thread scans before handing its cast to a warp
-#endif
-constexpr int kLongQueue = 64;  // queued casts per CTA (beyond: the thread finishes alone)
-
-struct LongCast {
-  double x, y;
-  int32_t a, idx;
-  uint32_t slot, pad;
-};
-
-// directional_cast (cddt.cpp:207-269) that stops after `cap` verification
-// windows: returns false with *next = the next candidate when it stopped
-// (cap < 0: no cap).
-__device__ __forceinline__ bool directional_cast_capped(const CddtView& c, double x, double y,
-                                                        int a, int cap, double* res, int* next) {
-  const int cxi = (int)floor(x), cyi = (int)floor(y);
-  *res = c.max_range;
-  if (!in_bounds(c, cxi, cyi)) return true;  // cddt.cpp:209
-  const QueryRow q = query_row(c, x, y, a);
-  RL_DCHECK(c, unsigned(cxi) < unsigned(c.w) && unsigned(cyi) < unsigned(c.h), 5);
-  const uint2 w0 = __ldg(&c.rowbits[cyi * c.wpr + (cxi >> 5)]);
-  if ((w0.x >> (cxi & 31)) & 1u) {  // cddt.cpp:210
-    *res = 0.0;
-    return true;
-  }
-  const double4 dir = c.dirs[a];
-  Walker<false> wk;
-  bool have_walker = false;
-  if (!((w0.y >> (cxi & 31)) & 1u)) {  // near field, cddt.cpp:225-232
-    wk.init_at(x, y, dir, 0.0);
-    have_walker = true;
-    const double r = wk.scan_to(c, kNearField);
-    if (r >= 0.0) {
-      *res = (c.max_range < r) ? c.max_range : r;
-      return true;
-    }
-    if (r == kWalkExit) return true;
-  }
-  const float* __restrict__ v = c.zp + q.lo;
-  const int n = (int)(q.hi - q.lo);
-  const RowSearch rs = partition_point_hinted(v, uint32_t(n), q.xq, q.forward, q.hint, q.hint2);
-  const int step = q.forward ? 1 : -1;
-  int windows = 0;
-  for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
-       idx += step) {
-    const double vv = (double)(uint32_t(idx) == rs.kidx ? rs.kval : __ldg(v + idx));
-    const double d = q.forward ? vv - q.xq : q.xq - vv;
-    if (d >= c.max_range) break;
-    int32_t cell;
-    if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {
-      *res = d;
-      return true;
-    }
-    if (windows == cap) {
-      *next = idx;  // this candidate's window is the first one not scanned
-      return false;
-    }
-    if (!have_walker) {
-      wk.init_at(x, y, dir, d - kVerifyHalf);
-      have_walker = true;
-    } else {
-      wk.seek(d - kVerifyHalf);
-    }
-    const double r = wk.scan_to(c, d + kVerifyHalf);
-    windows++;
-    if (r == kWalkExit) break;
-    if (r < 0.0) continue;
-    *res = d;
-    return true;
-  }
-  return true;
-}
-
-// The rest of a cast from candidate idx0 on, by all 32 lanes of a warp (the
-// arguments are warp-uniform): lane k takes candidate idx0 +- (32 j + k).
-__device__ __forceinline__ double resume_coop(const CddtView& c, double x, double y, int a,
-                                              int idx0) {
-  const QueryRow q = query_row(c, x, y, a);
-  const double4 dir = c.dirs[a];
-  const float* __restrict__ v = c.zp + q.lo;
-  const int n = (int)(q.hi - q.lo);
-  const int lane = threadIdx.x & 31, step = q.forward ? 1 : -1;
-  for (int base = idx0;; base += 32 * step) {
-    const int idx = base + lane * step;
-    int verdict = 0;  // 0: clean window, 1: settled at d, 2: the cast ends at max_range
-    double d = 0.0;
-    if (idx < 0 || idx >= n) {
-      verdict = 2;  // past the row's last candidate
-    } else {
-      const double vv = (double)__ldg(v + idx);
-      d = q.forward ? vv - q.xq : q.xq - vv;
-      int32_t cell;
-      if (d >= c.max_range) {
-        verdict = 2;
-      } else if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {
-        verdict = 1;
-      } else {
-        Walker<true> wk;
-        wk.init_at(x, y, dir, d - kVerifyHalf);
-        const double r = wk.scan_to(c, d + kVerifyHalf);
-        verdict = r == kWalkExit ? 2 : (r >= 0.0 ? 1 : 0);
-      }
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, verdict != 0);
-    if (m) {
-      const int first = __ffs(m) - 1;
-      const int vf = __shfl_sync(0xffffffffu, verdict, first);
-      const double df = __shfl_sync(0xffffffffu, d, first);
-      return vf == 1 ? df : c.max_range;
-    }
-  }
-}
-
 // Resident CTAs per SM: 4 (64 registers, a few bytes of spill) for the large
 // sets, where throughput decides (config 4); 3 (74 registers, no spill) for
 // the small ones, where the slowest cast decides (config 2: -3.5 %).
@@ -320,7 +188,7 @@ __global__ void __launch_bounds__(256, kSensorParticlesPerCta < 16 ? RL_SENSOR_M
     const double th = normalize_angle_2pi(pose[2][pl] + boff[b]);
     const int a = direction_index(th, c.K);
     double e;
-    int next, cap = RL_SENSOR_WCAP;
+    int next, cap = RL_COOP_WCAP;
     bool queued = false;
 #pragma unroll 1
     while (!directional_cast_capped(c, pose[0][pl], pose[1][pl], a, cap, &e, &next)) {
