@@ -450,8 +450,20 @@ def other_configs(device: int, rounds: int = 1000):
     flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}")
     ms2a = ev_time(lambda: rl.sensor_update(parts, m2, scan, spec, beam, table=table,
                                             degenerate=flag), 200)
+    # the same asynchronous update replayed from a CUDA graph (20 updates per graph)
+    side = torch.cuda.Stream(device)
+    side.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(side):
+        rl.sensor_update(parts, m2, scan, spec, beam, table=table, degenerate=flag)
+    torch.cuda.current_stream(device).wait_stream(side)
+    g2graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2graph):
+        for _ in range(20):
+            rl.sensor_update(parts, m2, scan, spec, beam, table=table, degenerate=flag)
+    ms2g = ev_time(g2graph.replay, 20) / 20
     out["config2"] = {"workload": "2000x2000 maze, theta_disc=120, max_range=500, 2500 particles x "
                                   "61 beams, 501x501 table",
+                      "ms_per_sensor_update_graphed": ms2g,
                       "ms_per_sensor_update": ms2a, "casts_per_s": 2500 * 61 / ms2a * 1e3,
                       "timing": "200 updates issued back to back through sensor_update(..., "
                                 "degenerate=<device flag>) (rl_sensor_update_async), CUDA events",
