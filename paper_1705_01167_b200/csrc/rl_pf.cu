@@ -135,12 +135,22 @@ __device__ __forceinline__ bool degenerate_sum(double s) {
 }
 
 // Tiled inclusive scan of the normalised weights. Tile j covers
-// [j*kScanTile, (j+1)*kScanTile); local[i] is the inclusive sum within the
-// tile and tile_excl[j] the sum of the earlier tile totals, so the cumulative
-// weight of particle i is tile_excl[i / kScanTile] + local[i]. With
-// normalise the input is w/S (or 1/n when S is degenerate) exactly as
-// k_normalize computes it.
-constexpr int kScanItems = 8, kScanTile = kPfThreads * kScanItems;
+// [j*T, (j+1)*T) with T = scan_tile_size(n) = 256 * ceil(n / 2^18), so there
+// are at most kMaxTiles tiles; local[i] is the inclusive sum within the tile
+// and tile_excl[j] the sum of the earlier tile totals, so the cumulative
+// weight of particle i is tile_excl[i / T] + local[i]. With normalise the
+// input is w/S (or 1/n when S is degenerate) exactly as k_normalize computes
+// it. Every path (fused step, stage entry points, any rank count with the
+// same n) runs these same fixed trees, so the cumulative weights agree bit
+// for bit.
+constexpr int kMaxTiles = 1024;
+
+__host__ __device__ __forceinline__ size_t scan_items(size_t n) {
+  return (n + size_t(kPfThreads) * kMaxTiles - 1) / (size_t(kPfThreads) * kMaxTiles);
+}
+__host__ __device__ __forceinline__ size_t scan_tile_size(size_t n) {
+  return size_t(kPfThreads) * (scan_items(n) ? scan_items(n) : 1);
+}
 
 struct ScanSmem {
   typename cub::BlockScan<double, kPfThreads>::TempStorage scan;
@@ -169,33 +179,35 @@ struct GatheredSet {
   __device__ __forceinline__ double gw(size_t i) const { return at(3, i); }
 };
 
+// One tile: each thread sums its ipt consecutive items sequentially, a block
+// exclusive scan of the thread totals, then each item's inclusive value is its
+// thread's prefix plus the running sum.
 template <class Set>
 __device__ __forceinline__ void scan_tile(const Set& ps, size_t n, size_t tile,
                                           bool normalise, double s, bool bad,
                                           double* __restrict__ local,
                                           double* __restrict__ tile_total, ScanSmem& sm) {
-  const size_t base = tile * kScanTile + size_t(threadIdx.x) * kScanItems;
-  double v[kScanItems];
-#pragma unroll
-  for (int k = 0; k < kScanItems; k++) {
-    const size_t i = base + k;
-    double a = 0.0;
-    if (i < n) {
-      const double wi = ps.gw(i);  // may come from another block of this grid
-      a = normalise ? (bad ? 1.0 / double(n) : wi / s) : wi;
-    }
-    v[k] = a;
+  const size_t ipt = scan_tile_size(n) / kPfThreads;
+  const size_t base = tile * scan_tile_size(n) + size_t(threadIdx.x) * ipt;
+  auto item = [&](size_t i) {
+    if (i >= n) return 0.0;
+    const double wi = ps.gw(i);  // may come from another block of this grid
+    return normalise ? (bad ? 1.0 / double(n) : wi / s) : wi;
+  };
+  double mine = 0.0;
+  for (size_t k = 0; k < ipt; k++) mine += item(base + k);
+  double pre, total;
+  cub::BlockScan<double, kPfThreads>(sm.scan).ExclusiveSum(mine, pre, total);
+  double run = pre;
+  for (size_t k = 0; k < ipt && base + k < n; k++) {
+    run += item(base + k);
+    local[base + k] = run;
   }
-  double total;
-  cub::BlockScan<double, kPfThreads>(sm.scan).InclusiveSum(v, v, total);
-#pragma unroll
-  for (int k = 0; k < kScanItems; k++)
-    if (base + k < n) local[base + k] = v[k];
   if (threadIdx.x == 0) tile_total[tile] = total;
 }
 
 // exclusive prefix of the tile totals by one warp: 32-wide Kogge-Stone scans
-// with a running carry (fixed association)
+// with a running carry (fixed association); tile_excl may be shared memory
 __device__ __forceinline__ void tile_prefix(const double* __restrict__ tile_total, size_t tiles,
                                             double* __restrict__ tile_excl) {
   const int lane = threadIdx.x & 31;
@@ -214,12 +226,33 @@ __device__ __forceinline__ void tile_prefix(const double* __restrict__ tile_tota
   }
 }
 
+// The comb's tile tables in shared memory: tile_excl (from global, or computed
+// here when tile_excl_g is null) and the tiles' end values excl + total. All
+// threads of the block call it.
+struct CombSmem {
+  double excl[kMaxTiles], end[kMaxTiles];
+};
+__device__ __forceinline__ void stage_tiles(const double* __restrict__ tile_total,
+                                            const double* __restrict__ tile_excl_g, size_t tiles,
+                                            CombSmem& cs) {
+  if (tile_excl_g) {
+    for (size_t t = threadIdx.x; t < tiles; t += blockDim.x) cs.excl[t] = __ldcg(tile_excl_g + t);
+  } else if (threadIdx.x < 32) {
+    tile_prefix(tile_total, tiles, cs.excl);
+  }
+  __syncthreads();
+  for (size_t t = threadIdx.x; t < tiles; t += blockDim.x)
+    cs.end[t] = cs.excl[t] + __ldcg(tile_total + t);
+  __syncthreads();
+}
+
 // slot m takes the first particle i with cumulative weight >= r + m/n,
-// capped at n-1 (the sequential comb of mcl.cpp:130-140)
+// capped at n-1 (the sequential comb of mcl.cpp:130-140): the tile by a
+// binary search over the tiles' end values in shared memory, then the
+// particle by a binary search within the tile.
 template <class Set>
-__device__ __forceinline__ void comb_slots(const double* __restrict__ local,
-                                           const double* __restrict__ tile_excl,
-                                           const Set& ps, size_t n,
+__device__ __forceinline__ void comb_slots(const double* __restrict__ local, const CombSmem& cs,
+                                           size_t tiles, const Set& ps, size_t n,
                                            size_t out_begin, size_t out_count,
                                            double* __restrict__ ox, double* __restrict__ oy,
                                            double* __restrict__ ot, double* __restrict__ ow,
@@ -227,21 +260,36 @@ __device__ __forceinline__ void comb_slots(const double* __restrict__ local,
   double u, unused;
   philox_uniform2(seed, kResampleStream, kResampleStream, iter, u, unused);
   const double r = (1.0 / double(n)) * u;  // uniform_real_distribution(0, 1/n)
+  const size_t T = scan_tile_size(n);
   for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < out_count;
        k += size_t(gridDim.x) * blockDim.x) {
     const size_t m = out_begin + k;
     const double target = r + double(m) / double(n);
-    size_t lo = 0, len = n;
+    size_t t = 0, len = tiles;
+    while (len > 0) {
+      const size_t half = len >> 1, mid = t + half;
+      if (cs.end[mid] < target) {
+        t = mid + 1;
+        len -= half + 1;
+      } else {
+        len = half;
+      }
+    }
+    if (t >= tiles) t = tiles - 1;
+    const double e = cs.excl[t];
+    const size_t base = t * T, cnt = (n - base < T) ? n - base : T;
+    size_t lo = 0;
+    len = cnt;
     while (len > 0) {
       const size_t half = len >> 1, mid = lo + half;
-      if (__ldcg(tile_excl + mid / kScanTile) + __ldcg(local + mid) < target) {
+      if (e + __ldcg(local + base + mid) < target) {
         lo = mid + 1;
         len -= half + 1;
       } else {
         len = half;
       }
     }
-    const size_t i = lo < n ? lo : n - 1;
+    const size_t i = base + lo < n ? base + lo : n - 1;
     ox[k] = ps.gx(i);
     oy[k] = ps.gy(i);
     ot[k] = ps.gt(i);
@@ -308,12 +356,15 @@ __global__ void __launch_bounds__(kPfThreads) k_tile_scan(
 }
 
 template <class Set>
-__global__ void k_comb(const double* __restrict__ local, const double* __restrict__ tile_excl,
-                       Set ps, size_t n, size_t out_begin,
-                       size_t out_count, double* __restrict__ ox, double* __restrict__ oy,
-                       double* __restrict__ ot, double* __restrict__ ow, uint64_t seed,
-                       uint64_t iter) {
-  comb_slots(local, tile_excl, ps, n, out_begin, out_count, ox, oy, ot, ow, seed, iter);
+__global__ void __launch_bounds__(kPfThreads) k_comb(
+    const double* __restrict__ local, const double* __restrict__ tile_total,
+    const double* __restrict__ tile_excl, Set ps, size_t n, size_t out_begin, size_t out_count,
+    double* __restrict__ ox, double* __restrict__ oy, double* __restrict__ ot,
+    double* __restrict__ ow, uint64_t seed, uint64_t iter) {
+  __shared__ CombSmem cs;
+  const size_t tiles = (n + scan_tile_size(n) - 1) / scan_tile_size(n);
+  stage_tiles(tile_total, tile_excl, tiles, cs);
+  comb_slots(local, cs, tiles, ps, n, out_begin, out_count, ox, oy, ot, ow, seed, iter);
 }
 
 // Mcl::estimate (mcl.cpp:176-187) from the weight moments of the step:
@@ -387,16 +438,18 @@ __global__ void __launch_bounds__(kPfThreads, 2) k_pf_finish(FinishArgs a) {
   }
   // 3. normalised tile scans
   __shared__ ScanSmem sm;
-  const size_t tiles = (n + kScanTile - 1) / kScanTile;
+  const size_t tiles = (n + scan_tile_size(n) - 1) / scan_tile_size(n);
   for (size_t j = blockIdx.x; j < tiles; j += gridDim.x) {
     scan_tile(PlainSet{a.x, a.y, a.t, a.w}, n, j, true, S, bad, a.local, a.tile_total, sm);
     __syncthreads();
   }
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x < 32) tile_prefix(a.tile_total, tiles, a.tile_excl);
-  grid.sync();
-  // 4. comb into the scratch set, then copy back over the caller's arrays
-  comb_slots(a.local, a.tile_excl, PlainSet{a.x, a.y, a.t, a.w}, n, 0, n, a.nxyzw, a.nxyzw + n,
+  // 4. every block computes the tile prefix itself (the same fixed tree as the
+  // stage path's), so no further grid sync; comb into the scratch set, then
+  // copy back over the caller's arrays
+  __shared__ CombSmem cs;
+  stage_tiles(a.tile_total, nullptr, tiles, cs);
+  comb_slots(a.local, cs, tiles, PlainSet{a.x, a.y, a.t, a.w}, n, 0, n, a.nxyzw, a.nxyzw + n,
              a.nxyzw + 2 * n, a.nxyzw + 3 * n, a.seed, a.iter);
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.gmax_key = 0;  // ready for the next step
@@ -437,7 +490,7 @@ static int blocks(size_t n, int threads = 256, int per_sm = 8) {
 // shared by every path so the sums agree bit for bit
 static int moment_blocks(size_t n) { return blocks(n, kPfThreads, 2); }
 
-static size_t scan_tiles(size_t n) { return (n + kScanTile - 1) / kScanTile; }
+static size_t scan_tiles(size_t n) { return (n + scan_tile_size(n) - 1) / scan_tile_size(n); }
 
 static MotionArgs motion_args(double dx, double dy, double dth, const rl_motion_noise_t* noise,
                               uint64_t seed, uint64_t iter, uint64_t offset) {
@@ -539,8 +592,8 @@ int rl_resample_low_variance(const double* x, const double* y, const double* the
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   const PlainSet ps{x, y, theta, w};
   k_tile_scan<<<int(T), kPfThreads, 0, s>>>(ps, n, local, tile_total, tile_excl, ticket);
-  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, ps, n, out_begin, out_count,
-                                          ox, oy, otheta, ow, seed, iteration);
+  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_total, tile_excl, ps, n, out_begin,
+                                          out_count, ox, oy, otheta, ow, seed, iteration);
   RL_CK(cudaGetLastError());
   RL_TRY(scratch_free(local, s));
   if (!stream) RL_CK(cudaStreamSynchronize(s));
@@ -635,7 +688,7 @@ static int mcl_step_impl(rl_cddt* c, double* x, double* y, double* theta, double
     k_tile_scan<<<int(T), kPfThreads, 0, st>>>(ps, n, fa.local, fa.tile_total, fa.tile_excl,
                                                &ctl->ticket);
     if (est_dev) k_estimate<<<1, 1, 0, st>>>(mom->m, &mom->degenerate, n, est_dev);
-    k_comb<<<blocks(n), 256, 0, st>>>(fa.local, fa.tile_excl, ps, n, 0, n, fa.nxyzw,
+    k_comb<<<blocks(n), 256, 0, st>>>(fa.local, fa.tile_total, fa.tile_excl, ps, n, 0, n, fa.nxyzw,
                                       fa.nxyzw + n, fa.nxyzw + 2 * n, fa.nxyzw + 3 * n, seed,
                                       iteration);
     k_copy_back<<<blocks(n), 256, 0, st>>>(fa.nxyzw, x, y, theta, w, n, &ctl->gmax_key);
@@ -752,8 +805,8 @@ int rl_resample_gathered(const double* gathered, size_t n_local, int32_t world, 
   RL_CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
   const GatheredSet ps{gathered, n_local};
   k_tile_scan<<<int(T), kPfThreads, 0, s>>>(ps, n, local, tile_total, tile_excl, ticket);
-  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_excl, ps, n, out_begin, out_count, ox, oy,
-                                          otheta, ow, seed, iteration);
+  k_comb<<<blocks(out_count), 256, 0, s>>>(local, tile_total, tile_excl, ps, n, out_begin,
+                                          out_count, ox, oy, otheta, ow, seed, iteration);
   RL_CK(cudaGetLastError());
   RL_TRY(scratch_free(local, s));
   if (!stream) RL_CK(cudaStreamSynchronize(s));

@@ -100,6 +100,8 @@ class Mcl:
     on the device) selects the discretised likelihood T[m][e] instead of the
     analytic beam model."""
 
+    _RING = 16  # pinned estimate slots (steps that may be in flight)
+
     def __init__(self, method, cfg: MclConfig, table=None, inv_res: float = 1.0, group=None,
                  device=None, stages=None):
         import torch
@@ -137,7 +139,15 @@ class Mcl:
         self._scan_dev = torch.empty(cfg.scan.beam_count, **f64)
         self._bp = self.cfg.beam.c()
         self._noise = cfg.motion.c()
-        self.est_dev = torch.zeros(4, **f64)  # {x, y, theta, degenerate} of the last step
+        # {x, y, theta, degenerate} of each step. On a GPU the kernels write it straight into a
+        # ring of pinned host slots (device-visible under unified addressing): no copy operation
+        # on the stream; a slot is reused only after the step that last wrote it completed.
+        if self.dev.type == "cuda":
+            self._ring = torch.zeros((self._RING, 4), dtype=torch.float64, pin_memory=True)
+            self._ring_users = [None] * self._RING
+            self.est_dev = self._ring[0]
+        else:
+            self.est_dev = torch.zeros(4, **f64)
         # stage buffers of the sharded path
         self.logw = torch.empty(self.n_local, **f64)
         self.gmax = torch.empty(1, **f64)
@@ -190,7 +200,11 @@ class Mcl:
         if len(scan) != self.cfg.scan.beam_count:
             raise ValueError("scan length does not match beam count")  # mcl.cpp:61-62
         t0 = time.perf_counter()
-        if isinstance(scan, torch.Tensor):
+        scan_ptr = None
+        if (isinstance(scan, torch.Tensor) and scan.device == self.dev
+                and scan.dtype == torch.float64 and scan.is_contiguous()):
+            scan_ptr = scan.data_ptr()  # read in place, in stream order
+        elif isinstance(scan, torch.Tensor):
             self._scan_dev.copy_(scan, non_blocking=True)
         else:
             # through pinned memory: a pageable host->device copy would wait for the stream
@@ -198,14 +212,21 @@ class Mcl:
             if self.dev.type == "cuda":
                 src = src.pin_memory()
             self._scan_dev.copy_(src, non_blocking=True)
+        self._scan_ptr = scan_ptr if scan_ptr is not None else self._scan_dev.data_ptr()
         cuda = self.dev.type == "cuda"
         stream = torch_stream(self.dev) if cuda else None
         it = self.iteration
         self.iteration += 1
+        if cuda:  # this step's pinned estimate slot
+            k = it % self._RING
+            prev = self._ring_users[k]
+            if prev is not None:
+                prev._resolve()  # the step that last wrote the slot is done before it is reused
+            self.est_dev = self._ring[k]
         if self.world == 1 and self.stages is None:
             check(lib().rl_mcl_step_async(
                 self.cddt.handle, _p(self.x), _p(self.y), _p(self.theta), _p(self.weight),
-                self.n_local, odo_dx, odo_dy, odo_dtheta, _p(self._scan_dev),
+                self.n_local, odo_dx, odo_dy, odo_dtheta, self._scan_ptr,
                 self.cfg.scan.beam_count, self.cfg.scan.fov, C.byref(self._noise),
                 C.byref(self._bp), _p(self.table), self.zdim, self.inv_res, self.cfg.seed, it,
                 _p(self.est_dev), stream))
@@ -213,11 +234,10 @@ class Mcl:
             sharded_step(self, self.stages or CudaStages(self, stream), odo_dx, odo_dy,
                          odo_dtheta, it)
         if cuda:
-            host = torch.empty(4, dtype=torch.float64, pin_memory=True)
-            host.copy_(self.est_dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.dev))
-            r = MclStepResult(host, ev, time.perf_counter() - t0)
+            r = MclStepResult(self.est_dev, ev, time.perf_counter() - t0)
+            self._ring_users[k] = r
         else:
             r = MclStepResult(self.est_dev.clone(), None, time.perf_counter() - t0)
         self._last = r
@@ -236,7 +256,7 @@ class CudaStages:
         m = self.m
         check(lib().rl_pf_shard_sensor(
             m.cddt.handle, _p(m.x), _p(m.y), _p(m.theta), m.n_local, m.offset, dx, dy, dth,
-            C.byref(m._noise), m.cfg.seed, it, _p(m._scan_dev), m.cfg.scan.beam_count,
+            C.byref(m._noise), m.cfg.seed, it, m._scan_ptr, m.cfg.scan.beam_count,
             m.cfg.scan.fov, C.byref(m._bp), _p(m.table), m.zdim, m.inv_res, _p(m.logw),
             _p(m.gmax), self.stream))
 

@@ -59,6 +59,24 @@ scans = [torch.from_numpy(synth.scan(g, *pose[k + 1], 61, FOV, 500.0, 8.0, 0.05,
 host = []
 ms4 = timed(lambda k: host.append(f.step(*odo[k], scans[k]).seconds), iters)
 host_us = 1e6 * float(np.mean(host[5:]))
+# the same step through the raw C ABI (no Python Mcl bookkeeping), back to back
+import ctypes as C  # noqa: E402
+
+from paper_1705_01167_b200 import _lib  # noqa: E402
+L = _lib.lib()
+st = _lib.torch_stream(f.dev)
+est = torch.zeros(4, dtype=torch.float64, device="cuda")
+sptr = [s.data_ptr() for s in scans]
+
+
+def raw(k):
+    L.rl_mcl_step_async(f.cddt.handle, f.x.data_ptr(), f.y.data_ptr(), f.theta.data_ptr(),
+                        f.weight.data_ptr(), 40_000, *odo[k], sptr[k], 61, FOV, C.byref(f._noise),
+                        C.byref(f._bp), table.data_ptr(), 501, 1.0, 5, 10_000 + k, est.data_ptr(),
+                        st)
+
+
+ms4_raw = timed(raw, iters)
 lat = []
 for k in range(50):  # one step at a time, estimate read back
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -71,6 +89,7 @@ print(json.dumps(dict(lib=os.environ.get("RL_CDDT_LIB", "default"),
                       paired=os.environ.get("RL_SENSOR_PAIRED", "1"),
                       tail=os.environ.get("RL_SENSOR_TAIL_MAX", "default"),
                       paired_small=os.environ.get("RL_SENSOR_PAIRED_SMALL", "default"),
-                      cfg2_ms=ms2, cfg4_ms=ms4, cfg4_host_us_per_step=host_us,
+                      cfg2_ms=ms2, cfg4_ms=ms4, cfg4_raw_abi_ms=ms4_raw,
+                      cfg4_host_us_per_step=host_us,
                       cfg4_sync_ms_p50=float(np.median(lat)), w2_sum=float(w2.sum()),
                       est=[f.estimate().x, f.estimate().y])))
