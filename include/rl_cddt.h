@@ -7,7 +7,8 @@
  * interface it replaces (file:line relative to the reference tree). Plain
  * pointers and sizes only: no C++ or torch types cross this boundary, no
  * exceptions escape it. INTEGRATION.md shows the reference-side adapter
- * (a rangelib::RangeMethod subclass) and the ctypes binding.
+ * (a rangelib::RangeMethod subclass, include/rl_cddt_rangemethod.hpp; the
+ * particle filter rl_gpu::GpuMcl, include/rl_cddt_mcl.hpp) and the ctypes binding.
  *
  * Conventions
  *  - Geometry is in pixel units, angles in radians counter-clockwise from +x,

@@ -21,6 +21,7 @@
 #include "rangelib/raycast.hpp"
 #include "rangelib/rng.hpp"
 #include "rangelib/synthetic.hpp"
+#include "rl_cddt_mcl.hpp"
 #include "rl_cddt_rangemethod.hpp"
 
 using namespace rangelib;
@@ -220,9 +221,10 @@ static void acceptance_4() {
 // circles the map centre at radius 0.32 * min(w, h), 1.5 px per step, 200
 // steps; odometry corrupted by N(0, 1.5 px) / N(0, 0.04 rad); scans from the
 // reference's simulate_scan with sigma 6 px; re-seeded at the truth when the
-// error exceeds 20 px. The filter under test is the GPU one (rl_mcl_step:
-// motion, fused sensor model, estimate, resampling); the ray-marching and
-// LUT backends run the reference's own Mcl on the same sensor data.
+// error exceeds 20 px. The filter under test is the GPU one (rl_gpu::GpuMcl,
+// include/rl_cddt_mcl.hpp: rl_mcl_step's motion, fused sensor model,
+// estimate and resampling); the ray-marching and LUT backends run the
+// reference's own Mcl on the same sensor data.
 struct LoopResult {
   double median_error = 0.0;
   int resets = 0;
@@ -239,56 +241,39 @@ static void pose_on_loop(const OccupancyGrid& g, int step, double* x, double* y,
 
 static LoopResult run_loop(const OccupancyGrid& g, int K, const RangeMethod* ref_method,
                            bool gpu_prune, uint64_t seed) {
-  const int n = 1000, steps = 200;
-  ScanSpec spec;  // 61 beams, 270 degrees
+  const int steps = 200;
   const double step_px = 1.5, scan_sigma = 6.0, odo_t = 1.5, odo_r = 0.04;
-  MotionNoise mn;
-  mn.trans_per_trans = (1.25 * odo_t + 0.05) / step_px;
-  mn.rot_per_trans = (1.25 * odo_r + 0.002) / step_px;
-  BeamModelParams beam;
-  beam.sigma_hit = scan_sigma;
+  MclConfig fc;  // 1000 particles, 61 beams over 270 degrees
+  fc.particle_count = 1000;
+  fc.motion.trans_per_trans = (1.25 * odo_t + 0.05) / step_px;
+  fc.motion.rot_per_trans = (1.25 * odo_r + 0.002) / step_px;
+  fc.beam.sigma_hit = scan_sigma;
+  fc.seed = seed;
   RangeMethodConfig cfg;
   cfg.theta_disc = K;
+  // the filter under test: the reference's Mcl over a reference method, or
+  // rl_gpu::GpuMcl (include/rl_cddt_mcl.hpp) over the GPU structure
   std::unique_ptr<rl_gpu::GpuCddtMethod> gpu;
   std::unique_ptr<Mcl> cpu;
-  if (!ref_method) gpu = std::make_unique<rl_gpu::GpuCddtMethod>(g, cfg, gpu_prune);
-  const double mr = ref_method ? ref_method->max_range() : gpu->max_range();
-  beam.z_max = mr;
+  std::unique_ptr<rl_gpu::GpuMcl> gmcl;
   if (ref_method) {
-    MclConfig fc;
-    fc.particle_count = n;
-    fc.motion = mn;
-    fc.beam = beam;
-    fc.seed = seed;
     cpu = std::make_unique<Mcl>(*ref_method, fc);
+  } else {
+    gpu = std::make_unique<rl_gpu::GpuCddtMethod>(g, cfg, gpu_prune);
+    gmcl = std::make_unique<rl_gpu::GpuMcl>(*gpu, fc);
   }
-  Dev<double> px(n), py(n), pt(n), pw(n), dscan(spec.beam_count);
-  std::mt19937_64 init_rng(seed * 7 + 1);
+  const double mr = ref_method ? ref_method->max_range() : gpu->max_range();
   auto seed_at = [&](double x, double y, double th) {
-    if (cpu) {
+    if (cpu)
       cpu->init_gaussian(x, y, th, 2.0, 0.1);
-      return;
-    }
-    std::normal_distribution<double> gxy(0.0, 2.0), gth(0.0, 0.1);
-    std::vector<double> hx(n), hy(n), ht(n), hw(n, 1.0 / n);
-    for (int i = 0; i < n; i++) {
-      hx[i] = x + gxy(init_rng);
-      hy[i] = y + gxy(init_rng);
-      ht[i] = normalize_angle_2pi(th + gth(init_rng));
-    }
-    px.put(hx);
-    py.put(hy);
-    pt.put(ht);
-    pw.put(hw);
+    else
+      gmcl->init_gaussian(x, y, th, 2.0, 0.1);
   };
   std::mt19937_64 world(seed ^ 0x9e3779b97f4a7c15ull);
   std::normal_distribution<double> nt(0.0, odo_t), nr(0.0, odo_r);
   double tx, ty, tth;
   pose_on_loop(g, 0, &tx, &ty, &tth);
   seed_at(tx, ty, tth);
-  rl_motion_noise_t noise{mn.trans_per_trans, mn.trans_per_rot, mn.rot_per_rot, mn.rot_per_trans};
-  rl_beam_params_t bp{beam.w_hit, beam.w_short, beam.w_max, beam.w_rand, beam.sigma_hit,
-                      beam.lambda_short, beam.z_max};
   std::vector<double> errs;
   LoopResult res;
   for (int step = 1; step <= steps; step++) {
@@ -301,23 +286,9 @@ static LoopResult run_loop(const OccupancyGrid& g, int K, const RangeMethod* ref
     ty = ny;
     tth = nth;
     const double ox = dx + nt(world), oy = dy + nt(world), oth = dth + nr(world);
-    std::vector<double> scan = simulate_scan(g, tx, ty, tth, spec, mr, scan_sigma, world);
-    double ex, ey;
-    if (cpu) {
-      MclStepResult r = cpu->step(ox, oy, oth, scan);
-      ex = r.estimate.x;
-      ey = r.estimate.y;
-    } else {
-      dscan.put(scan);
-      double est[3];
-      const int st = rl_mcl_step(gpu->handle(), px.p, py.p, pt.p, pw.p, n, ox, oy, oth, dscan.p,
-                                 spec.beam_count, spec.fov, &noise, &bp, nullptr, 0, 1.0, seed,
-                                 uint64_t(step), est, nullptr);
-      if (st != RL_OK && st != RL_EDEGENERATE) rl_gpu::throw_on(st);
-      ex = est[0];
-      ey = est[1];
-    }
-    const double err = std::hypot(ex - tx, ey - ty);
+    std::vector<double> scan = simulate_scan(g, tx, ty, tth, fc.scan, mr, scan_sigma, world);
+    const MclStepResult r = cpu ? cpu->step(ox, oy, oth, scan) : gmcl->step(ox, oy, oth, scan);
+    const double err = std::hypot(r.estimate.x - tx, r.estimate.y - ty);
     if (step > 10) errs.push_back(err);
     if (err > 20.0) {
       seed_at(tx, ty, tth);
