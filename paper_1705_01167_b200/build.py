@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -67,7 +68,7 @@ def build_cuda(force: bool = False, defines: tuple[str, ...] = (), out: Path | N
     if not defines and out is None:
         objdir = OBJ
     else:  # variant libraries keep their own objects
-        tag = "_".join(d.replace("=", "") for d in defines) or Path(out).stem
+        tag = "_".join(re.sub(r"[^A-Za-z0-9_]", "", d) for d in defines) or Path(out).stem
         objdir = OBJ / ("v_" + tag)
     objdir.mkdir(parents=True, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
