@@ -367,6 +367,18 @@ def pf_update_timing(iterations: int, device: int, group=None):
                           device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX, group=group)
         times = tt.cpu().numpy()
+    peak, peak_kind = measured_hbm_peak()
+    ss = json.loads((ROOT / "profiles" / "sensor_sectors.json").read_text())["config4"]
+    b_step = 40_000 * (61 * 32.0 * ss["sectors_per_beam"] + 96.0)
+    ach = b_step / (float(np.median(times)) * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "peak_source": f"{peak_kind} hbm_gbs",
+            "algorithmic_bytes_per_step": b_step,
+            "sectors_per_beam": ss["sectors_per_beam"],
+            "definition": "SURVEY.md §8d: per particle 61 * 32 * S-bar_beam + 96 B (S-bar_beam from "
+                          "the instrumented restatement, profiles/sensor_sectors.json); the sensor "
+                          "kernel's working set is cache-resident and it is issue-bound (ncu), so "
+                          "this measures how fast the reference's traffic is served"}
     return {"workload": "BASELINE config 4: 40,000 particles x 61 beams, 2000x2000 maze, "
                         f"theta_disc=120, 501x501 table, {world} GPU"
                         + (f"s (particles sharded, {40_000 // world} per GPU; max over ranks)"
@@ -378,6 +390,7 @@ def pf_update_timing(iterations: int, device: int, group=None):
                       "updates; ms_per_update_synchronous_p50: one update at a time with its "
                       "estimate read back (host launch latency included)",
             "ms_per_update_synchronous_p50": float(np.median(lat)),
+            "roofline": roof,
             "casts_per_update": 40_000 * 61,
             "median_position_error_px": float(np.median(errs[10:]))}
 
@@ -461,8 +474,18 @@ def other_configs(device: int, rounds: int = 1000):
         for _ in range(20):
             rl.sensor_update(parts, m2, scan, spec, beam, table=table, degenerate=flag)
     ms2g = ev_time(g2graph.replay, 20) / 20
+    peak, peak_kind = measured_hbm_peak()
+    s2 = json.loads((ROOT / "profiles" / "sensor_sectors.json").read_text())["config2"]
+    b_upd = 2500 * (61 * 32.0 * s2["sectors_per_beam"] + 20.0)
+    ach2 = b_upd / (ms2a * 1e-3) / 1e9
     out["config2"] = {"workload": "2000x2000 maze, theta_disc=120, max_range=500, 2500 particles x "
                                   "61 beams, 501x501 table",
+                      "roofline": {"bound": "hbm", "achieved": ach2, "peak": peak, "unit": "GB/s",
+                                   "frac": ach2 / peak, "peak_source": f"{peak_kind} hbm_gbs",
+                                   "algorithmic_bytes_per_update": b_upd,
+                                   "sectors_per_beam": s2["sectors_per_beam"],
+                                   "definition": "SURVEY.md §8d: per beam 32 * S-bar_beam + 20/61 B; "
+                                                 "one-wave, latency-bound launch"},
                       "ms_per_sensor_update_graphed": ms2g,
                       "ms_per_sensor_update": ms2a, "casts_per_s": 2500 * 61 / ms2a * 1e3,
                       "timing": "200 updates issued back to back through sensor_update(..., "
