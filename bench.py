@@ -250,9 +250,22 @@ def reference_cpu_configs(threads: int, mcl_iterations: int = 10) -> dict:
     for _ in range(reps):
         r2.sensor_update(px, py, pt, scan, 4.71238898038469, params, paired=True)
     ms2 = (time.perf_counter() - t0) / reps * 1e3
+    # the table model through the restatement (oracle/cddt_oracle.c, a port), one thread
+    from paper_1705_01167_b200 import rangelib
+    tab = rangelib.beam_table(rangelib.BeamModelParams(sigma_hit=8.0, z_max=500.0), 501, 1.0)
+    o2 = oracle.OracleCddt(g2, 120, 500.0)
+    o2.sensor_update(px, py, pt, scan, 4.71238898038469, params, table=tab, threads=1)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        o2.sensor_update(px, py, pt, scan, 4.71238898038469, params, table=tab, threads=1)
+    port = {"ms_per_sensor_update": (time.perf_counter() - t0) / reps * 1e3, "threads": 1}
+    del o2
     out["config2"] = {"ms_per_sensor_update": ms2, "casts_per_s": 2500 * 61 / ms2 * 1e3,
                       "threads": 1, "model": "analytic beam_likelihood (no table path in the "
-                                               "reference)", "paired_casts": True}
+                                               "reference)", "paired_casts": True,
+                      "table_model_port": dict(port, kind="port",
+                                               what="the 501x501 table model through the C "
+                                                    "restatement (oracle/cddt_oracle.c)")}
     x0, y0, t0_ = synth.free_pose(g2, 15, seed=8)
     pose, odo = synth.trajectory(g2, x0, y0, t0_, mcl_iterations, 1.0, 15.0, seed=4)
     scans = np.stack([synth.scan(g2, *pose[k + 1], 61, 4.71238898038469, 500.0, 8.0, 0.05,
