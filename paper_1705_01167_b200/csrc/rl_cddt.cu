@@ -671,6 +671,7 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->pf_ctl.release();
     if (c->pf_host) cudaFreeHost(c->pf_host);
     if (c->host_small) cudaFreeHost(c->host_small);
+    if (c->upd_host) cudaFreeHost(c->upd_host);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->counted) handle_closed(c->dev);
   }

@@ -137,6 +137,8 @@ struct rl_cddt {
   void* pf_host = nullptr;          // fused PF step: pinned host copy of the moments
   uint32_t* host_small = nullptr;   // 64 pinned bytes for small read-backs (flags, counts)
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
+  void* upd_host = nullptr;         // incremental edits: pinned staging for the uploads
+  size_t upd_host_n = 0;
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off
 

@@ -11,14 +11,16 @@
 //   2. host: recompute occupancy/clear/membership flags in the 1-cell dilation
 //      of those cells; cells whose membership flipped are the delta pixels;
 //   3. device: expand delta pixels to (row, value, +/-1) records over all
-//      slices, radix-sort them by (row, value);
-//   4. device: new row lengths -> scan -> per-row merge of the old sorted row
-//      with its sorted deltas (unaffected rows are a straight copy).
-// Only O(changed pixels * S) records are sorted; the copy is one pass over
+//      slices, counted per row; one scan gives both the new row offsets and
+//      each row's bucket of delta records, which a second pass fills;
+//   4. device: per-row merge of the old sorted row with its (unsorted)
+//      deltas (unaffected rows are a straight copy).
+// Only O(changed pixels * S) records are written; the copy is one pass over
 // the zero-point array.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
 #include <unordered_map>
 
 #include "rl_common.cuh"
@@ -43,18 +45,48 @@ __device__ __forceinline__ void pixel_rows_u(const SliceParam& sp, int px, int p
   v = __double2float_rn(cx * sp.cos_t + cy * sp.sin_t);
 }
 
-// order-preserving map f32 -> u32 (negatives flipped)
-__device__ __forceinline__ uint32_t f2key(float f) {
-  uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+// delta pixel (cell, sign) x slice -> per-row counts of added / removed points
+__global__ void k_delta_count(const int32_t* __restrict__ cells, const int8_t* __restrict__ sign,
+                              int n_cells, const SliceParam* __restrict__ slices, int S, int w,
+                              int32_t* __restrict__ add_cnt, int32_t* __restrict__ rem_cnt) {
+  const int total = n_cells * S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int k = i / S, s = i % S;
+    const int cell = cells[k];
+    const SliceParam sp = slices[s];
+    int r0, r1;
+    float v;
+    pixel_rows_u(sp, cell % w, cell / w, r0, r1, v);
+    int32_t* cnt = sign[k] > 0 ? add_cnt : rem_cnt;
+    for (int r = r0; r <= r1; r++) atomicAdd(&cnt[sp.row_base + uint32_t(r)], 1);
+  }
 }
 
-// delta pixel (cell, sign) x slice -> records key = row<<32 | f2key(v), val = sign
-__global__ void k_delta_records(const int32_t* __restrict__ cells, const int8_t* __restrict__ sign,
+// packed[g] = (deltas of row g) << 32 | (new length of row g); packed[rows] = 0.
+// One exclusive scan of it gives the new CSR offsets (low word) and the start
+// of each row's delta bucket (high word).
+__global__ void k_pack_len(const uint32_t* __restrict__ off, const int32_t* __restrict__ add_cnt,
+                           const int32_t* __restrict__ rem_cnt,
+                           unsigned long long* __restrict__ packed, size_t rows) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
+       g += size_t(gridDim.x) * blockDim.x) {
+    if (g == rows) {
+      packed[g] = 0ull;
+      continue;
+    }
+    const uint32_t len = (off[g + 1] - off[g]) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]);
+    const uint32_t nd = uint32_t(add_cnt[g] + rem_cnt[g]);
+    packed[g] = (static_cast<unsigned long long>(nd) << 32) | len;
+  }
+}
+
+// the delta records into their rows' buckets (order within a bucket is
+// arbitrary; the merge does not depend on it)
+__global__ void k_delta_scatter(const int32_t* __restrict__ cells, const int8_t* __restrict__ sign,
                                 int n_cells, const SliceParam* __restrict__ slices, int S, int w,
-                                unsigned long long* __restrict__ keys, int8_t* __restrict__ vals,
-                                unsigned* __restrict__ count, int32_t* __restrict__ add_cnt,
-                                int32_t* __restrict__ rem_cnt) {
+                                const unsigned long long* __restrict__ packed_off,
+                                uint32_t* __restrict__ cursor, float* __restrict__ rec_v,
+                                int8_t* __restrict__ rec_s) {
   const int total = n_cells * S;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int k = i / S, s = i % S;
@@ -65,28 +97,11 @@ __global__ void k_delta_records(const int32_t* __restrict__ cells, const int8_t*
     pixel_rows_u(sp, cell % w, cell / w, r0, r1, v);
     for (int r = r0; r <= r1; r++) {
       const uint32_t g = sp.row_base + uint32_t(r);
-      unsigned pos = atomicAdd(count, 1u);
-      keys[pos] = (static_cast<unsigned long long>(g) << 32) | f2key(v);
-      vals[pos] = sign[k];
-      if (sign[k] > 0)
-        atomicAdd(&add_cnt[g], 1);
-      else
-        atomicAdd(&rem_cnt[g], 1);
+      const uint32_t pos = uint32_t(packed_off[g] >> 32) + atomicAdd(&cursor[g], 1u);
+      rec_v[pos] = v;
+      rec_s[pos] = sign[k];
     }
   }
-}
-
-__global__ void k_new_len(const uint32_t* __restrict__ off, const int32_t* __restrict__ add_cnt,
-                          const int32_t* __restrict__ rem_cnt, uint32_t* __restrict__ len,
-                          size_t rows) {
-  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
-       g += size_t(gridDim.x) * blockDim.x)
-    len[g] = g < rows ? (off[g + 1] - off[g]) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]) : 0u;
-}
-
-__device__ __forceinline__ float key2f(unsigned long long key) {
-  const uint32_t k = uint32_t(key);
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
 // first index in v[0, n) whose value is > x (upper) or >= x (lower)
@@ -106,30 +121,35 @@ __device__ __forceinline__ uint32_t row_bound(const float* __restrict__ v, uint3
   return lo;
 }
 
-// Merge each row's sorted delta records into its zero points, one warp per
-// row (Cddt::add/remove_pixel_points: insert keeps the row sorted, remove
-// drops one equal element; cddt.cpp:332-377, cddt.hpp:67-84). Equal values are
+// Merge each row's delta records into its zero points, one warp per row
+// (Cddt::add/remove_pixel_points: insert keeps the row sorted, remove drops
+// one equal element; cddt.cpp:332-377, cddt.hpp:67-84). Equal values are
 // identical floats, so the merged row is the sorted multiset
 //   old - removed copies + added values,
-// which a warp builds in parallel for rows with at most 32 records: every
-// remove claims the next unclaimed copy of its value; a kept old element
-// lands at (its index - removed before it + adds smaller than it); an add
-// lands after the kept copies <= its value and the adds before it. Rows with
-// more records fall back to a sequential merge by lane 0.
+// which a warp builds in parallel for rows with at most 32 records, in any
+// order: every remove claims the next unclaimed copy of its value (ranked
+// among the equal removes by lane); a kept old element lands at (its index -
+// removed before it + adds smaller than it); an add lands after the kept
+// copies <= its value, the smaller adds and the equal adds of lower lanes.
+// Rows with more records: lane 0 sorts the bucket by value and merges
+// sequentially. Also writes the new CSR offsets (low word of packed_off).
 __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* __restrict__ old_zp,
-                             const uint32_t* __restrict__ new_off, float* __restrict__ new_zp,
+                             const unsigned long long* __restrict__ packed_off,
+                             uint32_t* __restrict__ new_off_out, float* __restrict__ new_zp,
                              const int32_t* __restrict__ add_cnt,
-                             const int32_t* __restrict__ rem_cnt,
-                             const unsigned long long* __restrict__ keys,
-                             const int8_t* __restrict__ vals, unsigned n_rec, size_t rows,
+                             const int32_t* __restrict__ rem_cnt, float* __restrict__ rec_v,
+                             int8_t* __restrict__ rec_s, size_t rows,
                              unsigned* __restrict__ unmatched) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
   const size_t warp = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
   const size_t nwarps = (size_t(gridDim.x) * blockDim.x) >> 5;
+  if (warp == 0 && lane == 0) new_off_out[rows] = uint32_t(packed_off[rows]);
   for (size_t g = warp; g < rows; g += nwarps) {
     const uint32_t a = old_off[g], b = old_off[g + 1];
-    const uint32_t o = new_off[g];
+    const unsigned long long po = packed_off[g];
+    const uint32_t o = uint32_t(po);
+    if (lane == 0) new_off_out[g] = o;
     const unsigned nd = unsigned(add_cnt[g] + rem_cnt[g]);
     if (nd == 0) {  // unchanged row: copy, four loads in flight per lane
       uint32_t i = a + lane;
@@ -145,29 +165,13 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
       for (; i < b; i += 32) new_zp[o + (i - a)] = __ldcs(old_zp + i);
       continue;
     }
-    // delta range of row g: lower_bound of g<<32 in the sorted keys (lane 0)
-    unsigned j0 = 0;
-    if (lane == 0) {
-      const unsigned long long lo_key = static_cast<unsigned long long>(g) << 32;
-      unsigned lo = 0, len = n_rec;
-      while (len > 0) {
-        const unsigned half = len >> 1, mid = lo + half;
-        if (keys[mid] < lo_key) {
-          lo = mid + 1;
-          len -= half + 1;
-        } else {
-          len = half;
-        }
-      }
-      j0 = lo;
-    }
-    j0 = __shfl_sync(0xffffffffu, j0, 0);
+    const unsigned j0 = unsigned(po >> 32);  // this row's delta bucket
     const float* __restrict__ row = old_zp + a;
     const uint32_t n = b - a;
     if (nd <= 32) {
       const bool has = lane < nd;
-      const float dv = has ? key2f(keys[j0 + lane]) : 0.f;
-      const bool add = has && vals[j0 + lane] > 0, rem = has && !add;
+      const float dv = has ? rec_v[j0 + lane] : 0.f;
+      const bool add = has && rec_s[j0 + lane] > 0, rem = has && !add;
       const unsigned add_mask = __ballot_sync(0xffffffffu, add);
       const unsigned rem_mask = __ballot_sync(0xffffffffu, rem);
       // removes: the k-th remove of value v drops old copy lower_bound(v) + k
@@ -180,13 +184,14 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
         else
           atomicAdd(unmatched, 1u);
       }
-      // adds: after the kept copies <= dv and the adds sorted before this one
-      unsigned rem_le = 0;  // removed copies with value <= dv
+      // adds: after the kept copies <= dv, the smaller adds and the equal adds of lower lanes
+      unsigned rem_le = 0, adds_before = 0;
       for (unsigned l = 0; l < nd; l++) {
         const float dl = __shfl_sync(0xffffffffu, dv, l);
         rem_le += ((rem_mask >> l) & 1u) && !(dv < dl) ? 1u : 0u;
+        adds_before += ((add_mask >> l) & 1u) && (dl < dv || (dl == dv && l < lane)) ? 1u : 0u;
       }
-      if (add) new_zp[o + row_bound(row, n, dv, true) - rem_le + __popc(add_mask & lt)] = dv;
+      if (add) new_zp[o + row_bound(row, n, dv, true) - rem_le + adds_before] = dv;
       // kept old elements, 32 at a time
       for (uint32_t i0 = 0; i0 < n; i0 += 32) {
         const uint32_t i = i0 + lane;
@@ -205,16 +210,29 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
       continue;
     }
     if (lane != 0) continue;
-    // sequential merge for rows with many records
-    unsigned j = j0;
-    const unsigned jend = j0 + nd;
+    // many records: sort the bucket by value (insertion sort; equal values in
+    // any order give the same multiset), then merge sequentially
+    float* bv = rec_v + j0;
+    int8_t* bs = rec_s + j0;
+    for (unsigned x = 1; x < nd; x++) {
+      const float v = bv[x];
+      const int8_t sg = bs[x];
+      unsigned y = x;
+      for (; y > 0 && v < bv[y - 1]; y--) {
+        bv[y] = bv[y - 1];
+        bs[y] = bs[y - 1];
+      }
+      bv[y] = v;
+      bs[y] = sg;
+    }
+    unsigned j = 0;
     uint32_t i = a, w = o;
     unsigned miss = 0;
-    while (i < b || j < jend) {
-      if (j < jend) {
-        const float dv = key2f(keys[j]);
+    while (i < b || j < nd) {
+      if (j < nd) {
+        const float dv = bv[j];
         if (i == b || dv < old_zp[i]) {
-          if (vals[j] > 0)
+          if (bs[j] > 0)
             new_zp[w++] = dv;
           else
             miss++;
@@ -222,7 +240,7 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
           continue;
         }
         if (dv == old_zp[i]) {
-          if (vals[j] > 0) {
+          if (bs[j] > 0) {
             new_zp[w++] = dv;
           } else {
             i++;  // remove_one: drop one equal element
@@ -308,82 +326,91 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   cudaStream_t st = c->stream;
   const size_t nw = wcells.size();
   const int nd = int(dcells.size());
-  const size_t cap = size_t(nd) * c->S * 3;  // a unit square spans at most 3 rows
   const size_t rows = c->rows;
-  // one persistent workspace, carved in 256-byte aligned pieces
-  size_t sort_tmp = 0, scan_tmp = 0;
-  if (nd) {
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, (int8_t*)nullptr,
-                                    (int8_t*)nullptr, int(cap), 0, 64, st);
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  int(rows + 1), st);
-  }
+  size_t scan_tmp = 0;
+  if (nd)
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, int(rows + 1), st);
+  const size_t cap = size_t(nd) * c->S * 3;  // a unit square spans at most 3 rows
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd), 4 * rows, 4 * rows, 8 * cap,
-                          cap, 8 * cap, cap, 8, 4 * (rows + 1), std::max(sort_tmp, scan_tmp)};
+  // uploads wcells | wflags | dcells | dsign, staged through pinned memory so
+  // they go as one truly asynchronous copy
+  const size_t up_sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd)};
+  size_t up = 0;
+  for (size_t b : up_sizes) up += al(b);
+  // one persistent workspace, carved in 256-byte aligned pieces
+  const size_t sizes[] = {up, 12 * rows, 8 * (rows + 1), 8 * (rows + 1), 4 * cap, cap, 8, scan_tmp};
   size_t need = 0;
   for (size_t b : sizes) need += al(b);
   if (c->upd_ws.n < need) RL_TRY(c->upd_ws.alloc(need + need / 4));
+  if (c->upd_host_n < up) {
+    if (c->upd_host) cudaFreeHost(c->upd_host);
+    c->upd_host = nullptr;
+    c->upd_host_n = 0;
+    RL_CK(cudaMallocHost(&c->upd_host, up + up / 4));
+    c->upd_host_n = up + up / 4;
+  }
   uint8_t* cur = c->upd_ws.p;
   auto take = [&](size_t b) {
     uint8_t* p = cur;
     cur += al(b);
     return p;
   };
-  int32_t* d_wcells = reinterpret_cast<int32_t*>(take(sizes[0]));
-  uint8_t* d_wflags = take(sizes[1]);
-  int32_t* d_dcells = reinterpret_cast<int32_t*>(take(sizes[2]));
-  int8_t* d_dsign = reinterpret_cast<int8_t*>(take(sizes[3]));
-  int32_t* add_cnt = reinterpret_cast<int32_t*>(take(sizes[4]));
-  int32_t* rem_cnt = reinterpret_cast<int32_t*>(take(sizes[5]));
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(take(sizes[6]));
-  int8_t* vals = reinterpret_cast<int8_t*>(take(sizes[7]));
-  unsigned long long* keys_sorted = reinterpret_cast<unsigned long long*>(take(sizes[8]));
-  int8_t* vals_sorted = reinterpret_cast<int8_t*>(take(sizes[9]));
-  unsigned* d_count = reinterpret_cast<unsigned*>(take(sizes[10]));
-  uint32_t* len = reinterpret_cast<uint32_t*>(take(sizes[11]));
-  void* tmp = take(sizes[12]);
-
-  RL_CK(cudaMemcpyAsync(d_wcells, wcells.data(), 4 * nw, cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemcpyAsync(d_wflags, wflags.data(), nw, cudaMemcpyHostToDevice, st));
+  uint8_t* d_up = take(sizes[0]);
+  int32_t* add_cnt = reinterpret_cast<int32_t*>(take(sizes[1]));  // add | rem | cursor
+  int32_t* rem_cnt = add_cnt + rows;
+  uint32_t* cursor = reinterpret_cast<uint32_t*>(rem_cnt + rows);
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(take(sizes[2]));
+  unsigned long long* packed_off = reinterpret_cast<unsigned long long*>(take(sizes[3]));
+  float* rec_v = reinterpret_cast<float*>(take(sizes[4]));
+  int8_t* rec_s = reinterpret_cast<int8_t*>(take(sizes[5]));
+  unsigned* d_unmatched = reinterpret_cast<unsigned*>(take(sizes[6]));
+  void* tmp = take(sizes[7]);
+  size_t up_off[4];
+  {
+    uint8_t* hbuf = static_cast<uint8_t*>(c->upd_host);
+    const void* src[] = {wcells.data(), wflags.data(), dcells.data(), dsign.data()};
+    size_t o = 0;
+    for (int k = 0; k < 4; k++) {
+      up_off[k] = o;
+      if (up_sizes[k]) std::memcpy(hbuf + o, src[k], up_sizes[k]);
+      o += al(up_sizes[k]);
+    }
+    RL_CK(cudaMemcpyAsync(d_up, hbuf, up, cudaMemcpyHostToDevice, st));
+  }
+  const int32_t* d_wcells = reinterpret_cast<const int32_t*>(d_up + up_off[0]);
+  const uint8_t* d_wflags = d_up + up_off[1];
+  const int32_t* d_dcells = reinterpret_cast<const int32_t*>(d_up + up_off[2]);
+  const int8_t* d_dsign = reinterpret_cast<const int8_t*>(d_up + up_off[3]);
   k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(d_wcells, d_wflags, int(nw), c->flags.p);
   RL_CK(cudaGetLastError());
   RL_TRY(refresh_query_bits(c));
   if (nd == 0) return finish(c, nullptr);
 
-  // 3. delta records; unused key slots stay at UINT64_MAX and sort last, so
-  //    the fixed-size sort needs no host round trip for the record count
-  RL_CK(cudaMemcpyAsync(d_dcells, dcells.data(), 4 * size_t(nd), cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemcpyAsync(d_dsign, dsign.data(), size_t(nd), cudaMemcpyHostToDevice, st));
-  RL_CK(cudaMemsetAsync(add_cnt, 0, 4 * rows, st));
-  RL_CK(cudaMemsetAsync(rem_cnt, 0, 4 * rows, st));
-  RL_CK(cudaMemsetAsync(d_count, 0, 8, st));
-  RL_CK(cudaMemsetAsync(keys, 0xFF, 8 * cap, st));
-  k_delta_records<<<blocks_for(size_t(nd) * c->S, 256), 256, 0, st>>>(
-      d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, keys, vals, d_count, add_cnt, rem_cnt);
+  // 3. per-row delta counts -> one scan (new offsets | delta buckets) -> records into buckets
+  RL_CK(cudaMemsetAsync(add_cnt, 0, 12 * rows, st));
+  RL_CK(cudaMemsetAsync(d_unmatched, 0, 4, st));
+  const int db = blocks_for(size_t(nd) * c->S, 256);
+  k_delta_count<<<db, 256, 0, st>>>(d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, add_cnt,
+                                    rem_cnt);
+  k_pack_len<<<blocks_for(rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt, rem_cnt, packed,
+                                                        rows);
+  RL_CK(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp, packed, packed_off, int(rows + 1), st));
+  k_delta_scatter<<<db, 256, 0, st>>>(d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, packed_off,
+                                      cursor, rec_v, rec_s);
   RL_CK(cudaGetLastError());
-  // keys are row<<32 | value; the unused slots (all ones) must sort last, so
-  // the sort covers the value bits and enough row bits that no row is all ones
-  int row_bits = 1;
-  while ((size_t(1) << row_bits) <= rows) row_bits++;
-  RL_CK(cub::DeviceRadixSort::SortPairs(tmp, sort_tmp, keys, keys_sorted, vals, vals_sorted,
-                                        int(cap), 0, 32 + row_bits, st));
-  // 4. new offsets and merge into the spare buffers, then swap
+  // 4. merge into the spare buffers (the new offsets too), then swap
   if (c->off_spare.n < rows + 1) RL_TRY(c->off_spare.alloc(rows + 1));
   const size_t zp_need = c->zero_points + cap;
   if (c->zp_spare.n < zp_need) RL_TRY(c->zp_spare.alloc(zp_need + zp_need / 8));
-  uint32_t* new_off = c->off_spare.p;
-  k_new_len<<<blocks_for(rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt, rem_cnt, len, rows);
-  RL_CK(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp, len, new_off, int(rows + 1), st));
   k_merge_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(
-      c->row_off.p, c->zp.p, new_off, c->zp_spare.p, add_cnt, rem_cnt, keys_sorted, vals_sorted,
-      unsigned(cap), rows, d_count + 1);
+      c->row_off.p, c->zp.p, packed_off, c->off_spare.p, c->zp_spare.p, add_cnt, rem_cnt, rec_v,
+      rec_s, rows, d_unmatched);
   RL_CK(cudaGetLastError());
   uint32_t* total_miss = nullptr;  // pinned: {new zero-point total, missed removals}
   RL_TRY(host_small(c, &total_miss));
-  RL_CK(cudaMemcpyAsync(&total_miss[0], new_off + rows, 4, cudaMemcpyDeviceToHost, st));
-  RL_CK(cudaMemcpyAsync(&total_miss[1], d_count + 1, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaMemcpyAsync(&total_miss[0], packed_off + rows, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaMemcpyAsync(&total_miss[1], d_unmatched, 4, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
   if (total_miss[1]) {
     set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)",
