@@ -21,7 +21,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <unordered_map>
 
 #include "rl_common.cuh"
 
@@ -272,32 +271,35 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   const int w = c->w, h = c->h;
   auto at = [&](int x, int y) { return c->grid_h[size_t(y) * w + x] != 0; };
   auto inb = [&](int x, int y) { return x >= 0 && y >= 0 && x < w && y < h; };
-  // 1. replay in order; remember each touched cell's original state
-  std::unordered_map<int32_t, uint8_t> orig;
-  orig.reserve(n * 2);
-  for (size_t k = 0; k < n; k++) {
-    const int32_t cell = xy[2 * k + 1] * w + xy[2 * k];
-    orig.emplace(cell, c->grid_h[cell]);
-    c->grid_h[cell] = occ[k] ? 1 : 0;
-  }
+  // 1. the touched cells' original states, then replay in order (last writer
+  //    wins); changed = touched cells whose final state differs
+  std::vector<int32_t> touched(n);
+  for (size_t k = 0; k < n; k++) touched[k] = xy[2 * k + 1] * w + xy[2 * k];
+  std::sort(touched.begin(), touched.end());
+  touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+  std::vector<uint8_t> orig(touched.size());
+  for (size_t k = 0; k < touched.size(); k++) orig[k] = c->grid_h[touched[k]];
+  for (size_t k = 0; k < n; k++) c->grid_h[size_t(xy[2 * k + 1]) * w + xy[2 * k]] = occ[k] ? 1 : 0;
   std::vector<int32_t> changed;
-  for (auto& kv : orig)
-    if (kv.second != c->grid_h[kv.first]) changed.push_back(kv.first);
+  for (size_t k = 0; k < touched.size(); k++)
+    if (orig[k] != c->grid_h[touched[k]]) changed.push_back(touched[k]);
   if (changed.empty()) return RL_OK;
   // 2. flags in the dilation; membership deltas
-  std::unordered_map<int32_t, uint8_t> window;
+  std::vector<int32_t> window;
+  window.reserve(changed.size() * 9);
   for (int32_t cell : changed) {
     const int x = cell % w, y = cell / w;
     for (int dy = -1; dy <= 1; dy++)
       for (int dx = -1; dx <= 1; dx++)
-        if (inb(x + dx, y + dy)) window.emplace((y + dy) * w + (x + dx), 0);
+        if (inb(x + dx, y + dy)) window.push_back((y + dy) * w + (x + dx));
   }
+  std::sort(window.begin(), window.end());
+  window.erase(std::unique(window.begin(), window.end()), window.end());
   std::vector<int32_t> wcells, dcells;
   std::vector<uint8_t> wflags;
   std::vector<int8_t> dsign;
   wcells.reserve(window.size());
-  for (auto& kv : window) {
-    const int32_t cell = kv.first;
+  for (const int32_t cell : window) {
     const int x = cell % w, y = cell / w;
     const bool o = at(x, y);
     bool any_occ = false, any_free = false;
