@@ -120,6 +120,25 @@ __device__ __forceinline__ uint32_t row_bound(const float* __restrict__ v, uint3
   return lo;
 }
 
+// The row record of a merged row (cddt_device.cuh "Row records"): CSR range
+// and the probes of its first search levels, read back from the new row.
+__device__ __forceinline__ void write_row_record(float* __restrict__ hints, size_t g, uint32_t lo,
+                                                 const float* __restrict__ v, uint32_t n) {
+  float h[kHintFloats];
+  int slot = 0;
+  h[slot++] = __uint_as_float(lo);
+  h[slot++] = __uint_as_float(n);
+  for (int level = 0; level < kHintLevels; level++)
+    for (uint32_t path = 0; path < (1u << level) && slot < kHintFloats; path++, slot++) {
+      uint32_t idx;
+      h[slot] = hint_index(n, level, path, &idx) ? v[idx] : 0.f;
+    }
+  for (; slot < kHintFloats; slot++) h[slot] = 0.f;
+  for (int k = 0; k < kHintFloats; k += 4)
+    reinterpret_cast<float4*>(hints + g * kHintFloats)[k / 4] =
+        make_float4(h[k], h[k + 1], h[k + 2], h[k + 3]);
+}
+
 // Merge each row's delta records into its zero points, one warp per row
 // (Cddt::add/remove_pixel_points: insert keeps the row sorted, remove drops
 // one equal element; cddt.cpp:332-377, cddt.hpp:67-84). Equal values are
@@ -131,14 +150,16 @@ __device__ __forceinline__ uint32_t row_bound(const float* __restrict__ v, uint3
 // removed before it + adds smaller than it); an add lands after the kept
 // copies <= its value, the smaller adds and the equal adds of lower lanes.
 // Rows with more records: lane 0 sorts the bucket by value and merges
-// sequentially. Also writes the new CSR offsets (low word of packed_off).
+// sequentially. Also writes the new CSR offsets (low word of packed_off) and
+// the row records: an unchanged row only moves (its record's lo), a merged
+// row's record is rebuilt from the new row.
 __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* __restrict__ old_zp,
                              const unsigned long long* __restrict__ packed_off,
                              uint32_t* __restrict__ new_off_out, float* __restrict__ new_zp,
                              const int32_t* __restrict__ add_cnt,
                              const int32_t* __restrict__ rem_cnt, float* __restrict__ rec_v,
                              int8_t* __restrict__ rec_s, size_t rows,
-                             unsigned* __restrict__ unmatched) {
+                             unsigned* __restrict__ unmatched, float* __restrict__ hints) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
   const size_t warp = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
@@ -162,9 +183,11 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
         d[96] = v3;
       }
       for (; i < b; i += 32) new_zp[o + (i - a)] = __ldcs(old_zp + i);
+      if (lane == 0) hints[g * kHintFloats] = __uint_as_float(o);  // the record's lo
       continue;
     }
     const unsigned j0 = unsigned(po >> 32);  // this row's delta bucket
+    const uint32_t new_n = (b - a) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]);
     const float* __restrict__ row = old_zp + a;
     const uint32_t n = b - a;
     if (nd <= 32) {
@@ -206,6 +229,8 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
         }
         if (i < n && !removed) new_zp[o + i - rb + adds_lt] = e;
       }
+      __syncwarp();  // the warp's stores of the new row are visible to lane 0
+      if (lane == 0) write_row_record(hints, g, o, new_zp + o, new_n);
       continue;
     }
     if (lane != 0) continue;
@@ -251,6 +276,7 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
       new_zp[w++] = old_zp[i++];
     }
     if (miss) atomicAdd(unmatched, miss);
+    write_row_record(hints, g, o, new_zp + o, new_n);
   }
 }
 
@@ -407,7 +433,7 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
   if (c->zp_spare.n < zp_need) RL_TRY(c->zp_spare.alloc(zp_need + zp_need / 8));
   k_merge_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(
       c->row_off.p, c->zp.p, packed_off, c->off_spare.p, c->zp_spare.p, add_cnt, rem_cnt, rec_v,
-      rec_s, rows, d_unmatched);
+      rec_s, rows, d_unmatched, c->hints.p);
   RL_CK(cudaGetLastError());
   uint32_t* total_miss = nullptr;  // pinned: {new zero-point total, missed removals}
   RL_TRY(host_small(c, &total_miss));
@@ -420,8 +446,7 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
     return RL_ELOGIC;
   }
   std::swap(c->zp, c->zp_spare);
-  std::swap(c->row_off, c->off_spare);
-  RL_TRY(refresh_row_hints(c));
+  std::swap(c->row_off, c->off_spare);  // the row records were rewritten by k_merge_rows
   c->zero_points = total_miss[0];
   return finish(c, nullptr);
 }
