@@ -213,13 +213,14 @@ def reference_cpu(ref, qx, qy, qt, sample: int, threads: int, sample1: int):
     return r["out64"], dt, sample1 / sec1
 
 
-def reference_cpu_configs(threads: int, mcl_iterations: int = 10) -> dict:
-    """The reference's CPU paths beside BASELINE configs 1, 2 and 4 (the
+def reference_cpu_configs(threads: int, mcl_iterations: int = 10, cfg5_rounds: int = 20) -> dict:
+    """The reference's CPU paths beside BASELINE configs 1, 2, 4 and 5 (the
     unmodified rangelib in oracle/_ref, through its public API):
       config 1: Cddt build + 100k casts (one thread, thread cpu time; and all threads)
       config 2: sensor_update (mcl.cpp:58-120), 2,500 particles x 61 paired beams
       config 4: Mcl::step (mcl.cpp:189-201), 40,000 particles x 61 beams, a bounded
                 run of `mcl_iterations` steps (its own MclStepResult.seconds)
+      config 5: Cddt::set_occupancy over `cfg5_rounds` rounds of 50 random 3x3 blocks
     The reference's sensor model is the analytic beam_likelihood: it has no
     likelihood-table path, so configs 2 and 4 run the analytic model here."""
     import numpy as np
@@ -279,6 +280,23 @@ def reference_cpu_configs(threads: int, mcl_iterations: int = 10) -> dict:
                       "model": "analytic beam_likelihood (no table path in the reference)",
                       "what": "rangelib::Mcl::step (motion, paired-cast sensor model, estimate, "
                               "resampling), its own MclStepResult.seconds"}
+    del r2
+    # config 5: the same edit rounds (tests/golden/cfg5_rounds.json's seeds)
+    # through the reference's Cddt::set_occupancy, cell by cell in order
+    gold = json.loads((ROOT / "tests" / "golden" / "cfg5_rounds.json").read_text())
+    r5 = oracle.RefCddt(g2, 108, 0.0)
+    sec5 = []
+    for r in range(cfg5_rounds):
+        xy, occ = synth.block_edits(2000, 2000, 50, seed=gold["seed0"] + r)
+        st, sec = r5.set_occupancy_timed(xy, occ)
+        if st:
+            raise RuntimeError(f"reference set_occupancy failed ({st})")
+        sec5.append(sec)
+    out["config5"] = {"ms_per_update_round_p50": float(np.median(sec5)) * 1e3,
+                      "ms_per_update_round_mean": float(np.mean(sec5)) * 1e3,
+                      "rounds_timed": cfg5_rounds, "threads": 1,
+                      "what": "rangelib::Cddt::set_occupancy per edited cell (cddt.cpp:332-377), "
+                              "the first rounds of the bench's edit sequence, steady clock"}
     return out
 
 

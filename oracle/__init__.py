@@ -102,6 +102,8 @@ def ref_lib() -> C.CDLL:
         h.ref_directional_batch.argtypes = [_P, _P, _P, _P, _sz, _P]
         h.ref_cast_pair_batch.argtypes = [_P, _P, _P, _P, _sz, _P, _P]
         h.ref_set_occupancy.argtypes = [_P, C.c_int, C.c_int, C.c_int]
+        h.ref_set_occupancy_timed.argtypes = [_P, _P, _P, _sz, C.POINTER(C.c_int)]
+        h.ref_set_occupancy_timed.restype = _d
         h.ref_serialize.argtypes = [_P, _P, _sz]
         h.ref_serialize.restype = _sz
         h.ref_deserialize.argtypes = [_P, _sz, C.POINTER(_P)]
@@ -278,6 +280,14 @@ class RefCddt(_Base):
 
     def set_occupancy(self, x: int, y: int, occ: bool) -> int:
         return ref_lib().ref_set_occupancy(self._h, x, y, 1 if occ else 0)
+
+    def set_occupancy_timed(self, xy, occ) -> tuple[int, float]:
+        """Cddt::set_occupancy over a batch in order, in C++; (status, seconds)."""
+        xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
+        occ = np.ascontiguousarray(occ, np.uint8).reshape(-1)
+        st = C.c_int(0)
+        sec = ref_lib().ref_set_occupancy_timed(self._h, _p(xy), _p(occ), occ.size, C.byref(st))
+        return st.value, sec
 
     def export(self) -> dict:
         i = self.info()

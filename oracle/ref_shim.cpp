@@ -10,6 +10,7 @@
 // Used by tests/ to pin the C restatement (oracle/cddt_oracle.c) and the GPU
 // path, and by bench.py --impl reference / cpu_baseline as the reference's
 // own CPU implementation timed on the host cores.
+#include <chrono>
 #include <time.h>
 
 #include <cstdint>
@@ -217,6 +218,24 @@ int ref_set_occupancy(void* hp, int x, int y, int occ) {
   } catch (...) {
     return RS_EOTHER;
   }
+}
+
+// A batch of Cddt::set_occupancy calls (proj/src/cddt.cpp:332-377), the
+// reference's per-cell API in order, timed on the calling thread (steady
+// clock); stops at the first failing edit. Returns the seconds taken.
+double ref_set_occupancy_timed(void* hp, const int32_t* xy, const uint8_t* occ, size_t n,
+                               int* status) {
+  Cddt& c = static_cast<RefCddt*>(hp)->c;
+  *status = RS_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    for (size_t k = 0; k < n; k++) c.set_occupancy(xy[2 * k], xy[2 * k + 1], occ[k] != 0);
+  } catch (const std::logic_error& e) {
+    *status = dynamic_cast<const std::out_of_range*>(&e) ? RS_ERANGE : RS_ELOGIC;
+  } catch (...) {
+    *status = RS_EOTHER;
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 // serialize_cddt (proj/src/cddt.cpp:458-500); returns the byte size, copies

@@ -426,6 +426,8 @@ int build_structure(rl_cddt* c) {
     return RL_EINVAL;
   }
   c->zero_points = total;
+  c->zp_slots = total;  // dense rows
+  c->gapped = false;
 
   DevBuf<float> unsorted;
   RL_TRY(unsorted.alloc(total));
@@ -505,6 +507,7 @@ __global__ void k_remap_offsets(const uint32_t* __restrict__ old_off,
 
 int prune_structure(rl_cddt* c) {
   if (c->pruned) return RL_OK;
+  RL_TRY(densify_rows(c));  // prune reads dense rows (edits leave slack)
   cudaStream_t st = c->stream;
   const size_t n = c->zero_points;
   DevBuf<uint8_t> marks;
@@ -541,6 +544,7 @@ int prune_structure(rl_cddt* c) {
   c->zp = std::move(nzp);
   c->row_off = std::move(noff);
   c->zero_points = kept;
+  c->zp_slots = kept;
   c->pruned = true;
   RL_TRY(refresh_row_hints(c));
   RL_CK(cudaStreamSynchronize(st));
@@ -668,6 +672,11 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->upd_ws.release();
     c->zp_spare.release();
     c->off_spare.release();
+    c->row_len.release();
+    c->len_spare.release();
+    c->row_cap.release();
+    c->cap_spare.release();
+    c->bkt.release();
     c->pf_ctl.release();
     if (c->pf_host) cudaFreeHost(c->pf_host);
     if (c->host_small) cudaFreeHost(c->host_small);
@@ -701,7 +710,8 @@ int rl_cddt_info(const rl_cddt* c, rl_cddt_info_t* o) {
   const uint64_t wh = uint64_t(c->w) * c->h;
   o->memory_bytes = 4 * c->zero_points + (wh + 7) / 8 + uint64_t(c->S) * 48;  // cddt.hpp:200-203
   o->device_bytes = c->flags.bytes() + c->rowbits.bytes() + c->row_off.bytes() +
-                    c->hints.bytes() + 4 * c->zero_points + c->d_slices.bytes() +
+                    c->hints.bytes() + 4 * (c->gapped ? c->zp.n : c->zero_points) + c->row_len.bytes() + c->row_cap.bytes() +
+                    c->d_slices.bytes() +
                     c->d_dirs.bytes() + c->d_pdirs.bytes() + c->d_rbase.bytes();
   o->init_seconds = c->init_seconds;
   return RL_OK;
@@ -723,14 +733,33 @@ int rl_cddt_export(const rl_cddt* c, uint32_t* slice_row_base, uint64_t* row_off
     for (int s = 0; s < c->S; s++) slice_row_base[s] = c->slices[s].row_base;
     slice_row_base[c->S] = uint32_t(c->rows);
   }
-  if (row_off) {
-    std::vector<uint32_t> o(c->rows + 1);
+  if (c->gapped && (row_off || zp)) {  // slack rows: the dense CSR the reference defines
+    std::vector<uint32_t> o(c->rows + 1), len(c->rows);
+    std::vector<float> slots(c->zp_slots);
     RL_CK(cudaMemcpy(o.data(), c->row_off.p, sizeof(uint32_t) * (c->rows + 1),
                      cudaMemcpyDeviceToHost));
-    for (uint64_t i = 0; i <= c->rows; i++) row_off[i] = o[i];
+    RL_CK(cudaMemcpy(len.data(), c->row_len.p, sizeof(uint32_t) * c->rows,
+                     cudaMemcpyDeviceToHost));
+    if (zp && c->zp_slots)
+      RL_CK(cudaMemcpy(slots.data(), c->zp.p, sizeof(float) * c->zp_slots,
+                       cudaMemcpyDeviceToHost));
+    uint64_t at = 0;
+    for (uint64_t g = 0; g < c->rows; g++) {
+      if (row_off) row_off[g] = at;
+      if (zp) std::memcpy(zp + at, slots.data() + o[g], sizeof(float) * len[g]);
+      at += len[g];
+    }
+    if (row_off) row_off[c->rows] = at;
+  } else {
+    if (row_off) {
+      std::vector<uint32_t> o(c->rows + 1);
+      RL_CK(cudaMemcpy(o.data(), c->row_off.p, sizeof(uint32_t) * (c->rows + 1),
+                       cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i <= c->rows; i++) row_off[i] = o[i];
+    }
+    if (zp && c->zero_points)
+      RL_CK(cudaMemcpy(zp, c->zp.p, sizeof(float) * c->zero_points, cudaMemcpyDeviceToHost));
   }
-  if (zp && c->zero_points)
-    RL_CK(cudaMemcpy(zp, c->zp.p, sizeof(float) * c->zero_points, cudaMemcpyDeviceToHost));
   const size_t wh = size_t(c->w) * c->h;
   if (membership) std::memcpy(membership, c->member_h.data(), wh);
   if (grid) std::memcpy(grid, c->grid_h.data(), wh);

@@ -116,6 +116,8 @@ struct rl_cddt {
 
   std::vector<uint8_t> grid_h;    // host mirror: occupancy
   std::vector<uint8_t> member_h;  // host mirror: membership
+  std::vector<uint32_t> stamp;    // incremental edits: per-cell generation stamps (dedup)
+  uint32_t stamp_gen = 0;
 
   rl::DevBuf<uint8_t> flags;        // w*h
   rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
@@ -137,10 +139,24 @@ struct rl_cddt {
   void* pf_host = nullptr;          // fused PF step: pinned host copy of the moments
   uint32_t* host_small = nullptr;   // 64 pinned bytes for small read-backs (flags, counts)
   rl::DevBuf<uint8_t> upd_ws;       // incremental edits: scratch
+  rl::DevBuf<uint8_t> upd_up;       // incremental edits: the uploaded batch
   void* upd_host = nullptr;         // incremental edits: pinned staging for the uploads
   size_t upd_host_n = 0;
   rl::DevBuf<float> zp_spare;       // incremental edits: double buffer for zp
   rl::DevBuf<uint32_t> off_spare;   // incremental edits: double buffer for row_off
+  // Slack rows (set by the first edit batch, rl_update.cu): row g owns
+  // row_cap[g] slots of zp from row_off[g] (no longer monotone once rows move
+  // to the append area) and stores row_len[g] points there, so later edit
+  // batches merge only the rows they touch. Build, prune and load leave the
+  // rows dense (gapped = false, no row_len / row_cap).
+  bool gapped = false;
+  uint64_t zp_slots = 0;            // slots in use (rows + append area used): zero_points when dense
+  uint64_t slot_limit = 0;          // gapped: slots the append area may grow to (<= zp.n)
+  rl::DevBuf<uint32_t> row_len;     // gapped: points per row
+  rl::DevBuf<uint32_t> row_cap;     // gapped: slots per row
+  rl::DevBuf<uint32_t> len_spare;   // incremental edits: double buffers for row_len / row_cap
+  rl::DevBuf<uint32_t> cap_spare;
+  rl::DevBuf<uint8_t> bkt;          // incremental edits: per-row delta buckets (zeroed counts)
 
   rl::CddtView view() const {
     rl::CddtView v;
@@ -161,7 +177,7 @@ struct rl_cddt {
     v.max_range = max_range;
     v.chk = rl::check_counter(dev);
     v.n_rows = uint32_t(rows);
-    v.n_zp = uint32_t(zero_points);
+    v.n_zp = uint32_t(gapped ? zp_slots : zero_points);
     return v;
   }
 };
@@ -174,6 +190,7 @@ inline cudaStream_t pick_stream(const rl_cddt* c, void* s) {
 int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
+int densify_rows(rl_cddt* c);           // slack rows back to dense CSR (rl_update.cu)
 // stream-ordered scratch from the library's own per-device pool (rl_cddt.cu)
 int scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 int scratch_free(void* p, cudaStream_t st);

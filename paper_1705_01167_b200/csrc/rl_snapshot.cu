@@ -208,6 +208,8 @@ int rl_cddt_deserialize(const uint8_t* bytes, size_t n, int32_t device, rl_cddt*
     return fail(RL_EPARSE);
   }
   c->zero_points = zp.size();
+  c->zp_slots = zp.size();  // dense rows
+  c->gapped = false;
   // flags: occupancy and membership from the snapshot, clear mask rebuilt
   // (deserialize_cddt rebuilds it too, cddt.cpp:576-577)
   std::vector<uint8_t> flags(wh, 0);

@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "rl_common.cuh"
@@ -61,22 +62,40 @@ __global__ void k_delta_count(const int32_t* __restrict__ cells, const int8_t* _
   }
 }
 
-// packed[g] = (deltas of row g) << 32 | (new length of row g); packed[rows] = 0.
-// One exclusive scan of it gives the new CSR offsets (low word) and the start
-// of each row's delta bucket (high word).
-__global__ void k_pack_len(const uint32_t* __restrict__ off, const int32_t* __restrict__ add_cnt,
+// Slots a row of `len` points is given when the rows are (re)laid out by an
+// edit batch: room for later edits to merge in place (about 1/8 more).
+__host__ __device__ __forceinline__ uint32_t slot_capacity(uint32_t len) {
+  return len + (len >> 3) + 4u;
+}
+
+// packed[g] = (deltas of row g) << 32 | (slots of row g); packed[rows] = 0.
+// One exclusive scan of it gives the new row offsets (low word) and the start
+// of each row's delta bucket (high word). Also the new row lengths and their
+// sum (the new zero-point count).
+__global__ void k_pack_len(const uint32_t* __restrict__ off, const uint32_t* __restrict__ old_len,
+                           const int32_t* __restrict__ add_cnt,
                            const int32_t* __restrict__ rem_cnt,
-                           unsigned long long* __restrict__ packed, size_t rows) {
+                           unsigned long long* __restrict__ packed, uint32_t* __restrict__ new_len,
+                           uint32_t* __restrict__ new_cap, unsigned long long* __restrict__ total,
+                           size_t rows) {
+  unsigned long long sum = 0;
   for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
        g += size_t(gridDim.x) * blockDim.x) {
     if (g == rows) {
       packed[g] = 0ull;
       continue;
     }
-    const uint32_t len = (off[g + 1] - off[g]) + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]);
+    const uint32_t n0 = old_len ? old_len[g] : off[g + 1] - off[g];
+    const uint32_t len = n0 + uint32_t(add_cnt[g]) - uint32_t(rem_cnt[g]);
     const uint32_t nd = uint32_t(add_cnt[g] + rem_cnt[g]);
-    packed[g] = (static_cast<unsigned long long>(nd) << 32) | len;
+    packed[g] = (static_cast<unsigned long long>(nd) << 32) | slot_capacity(len);
+    new_len[g] = len;
+    new_cap[g] = slot_capacity(len);
+    sum += len;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(total, sum);
 }
 
 // the delta records into their rows' buckets (order within a bucket is
@@ -153,7 +172,8 @@ __device__ __forceinline__ void write_row_record(float* __restrict__ hints, size
 // sequentially. Also writes the new CSR offsets (low word of packed_off) and
 // the row records: an unchanged row only moves (its record's lo), a merged
 // row's record is rebuilt from the new row.
-__global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* __restrict__ old_zp,
+__global__ void k_merge_rows(const uint32_t* __restrict__ old_off,
+                             const uint32_t* __restrict__ old_len, const float* __restrict__ old_zp,
                              const unsigned long long* __restrict__ packed_off,
                              uint32_t* __restrict__ new_off_out, float* __restrict__ new_zp,
                              const int32_t* __restrict__ add_cnt,
@@ -166,7 +186,7 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
   const size_t nwarps = (size_t(gridDim.x) * blockDim.x) >> 5;
   if (warp == 0 && lane == 0) new_off_out[rows] = uint32_t(packed_off[rows]);
   for (size_t g = warp; g < rows; g += nwarps) {
-    const uint32_t a = old_off[g], b = old_off[g + 1];
+    const uint32_t a = old_off[g], b = old_len ? a + old_len[g] : old_off[g + 1];
     const unsigned long long po = packed_off[g];
     const uint32_t o = uint32_t(po);
     if (lane == 0) new_off_out[g] = o;
@@ -280,10 +300,35 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off, const float* 
   }
 }
 
-__global__ void k_set_flags(const int32_t* __restrict__ cells, const uint8_t* __restrict__ f,
-                            int n, uint8_t* __restrict__ flags) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    flags[cells[i]] = f[i];
+// The recomputed flags of the batch's dilation, and the same bits in the
+// query bitmaps (rowbits: per 32-cell word {occupied, clear}) — only the
+// words of the changed cells, by atomic bit updates.
+struct FlagEdits {
+  const int32_t* cells;
+  const uint8_t* f;
+  int n;
+};
+__device__ __forceinline__ void set_flag(const FlagEdits& fe, int i, int w, int wpr,
+                                         uint8_t* __restrict__ flags, uint2* __restrict__ bits) {
+  const int32_t cell = fe.cells[i];
+  const uint8_t f = fe.f[i];
+  flags[cell] = f;
+  const int x = cell % w, y = cell / w;
+  unsigned* word = reinterpret_cast<unsigned*>(bits + size_t(y) * wpr + (x >> 5));
+  const unsigned bit = 1u << (x & 31);
+  if (f & kOcc)
+    atomicOr(word, bit);
+  else
+    atomicAnd(word, ~bit);
+  if (f & kClear)
+    atomicOr(word + 1, bit);
+  else
+    atomicAnd(word + 1, ~bit);
+}
+__global__ void k_set_flags(FlagEdits fe, int w, int wpr, uint8_t* __restrict__ flags,
+                            uint2* __restrict__ bits) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fe.n; i += gridDim.x * blockDim.x)
+    set_flag(fe, i, w, wpr, flags, bits);
 }
 
 static int blocks_for(size_t work, int threads, int cap_per_sm = 16) {
@@ -292,19 +337,53 @@ static int blocks_for(size_t work, int threads, int cap_per_sm = 16) {
   return int(std::max<size_t>(1, std::min(b, cap)));
 }
 
+// The batch's membership deltas on the device: pixels and +1 (joins) / -1 (leaves).
+struct EditBatch {
+  const int32_t* cells;
+  const int8_t* sign;
+  int n;
+};
+static int edits_relayout(rl_cddt* c, const EditBatch& e);
+static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, unsigned* ctl,
+                          bool* applied);
+
 // Apply edits [0, n) (already validated) to the structure.
+#ifdef RL_EDIT_PROFILE
+#include <chrono>
+static double prof_now() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+#endif
 static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n) {
+#ifdef RL_EDIT_PROFILE
+  const double p0 = prof_now();
+#endif
   const int w = c->w, h = c->h;
   auto at = [&](int x, int y) { return c->grid_h[size_t(y) * w + x] != 0; };
   auto inb = [&](int x, int y) { return x >= 0 && y >= 0 && x < w && y < h; };
+  // cells are deduplicated with generation stamps (no sort: a batch touches
+  // a few thousand cells, and sorting them cost more than the GPU work)
+  if (c->stamp.size() != size_t(w) * h || c->stamp_gen > 0xfffffff0u) {
+    c->stamp.assign(size_t(w) * h, 0u);
+    c->stamp_gen = 0;
+  }
+  const uint32_t gen_t = ++c->stamp_gen, gen_w = ++c->stamp_gen;
+  uint32_t* stamp = c->stamp.data();
   // 1. the touched cells' original states, then replay in order (last writer
   //    wins); changed = touched cells whose final state differs
-  std::vector<int32_t> touched(n);
-  for (size_t k = 0; k < n; k++) touched[k] = xy[2 * k + 1] * w + xy[2 * k];
-  std::sort(touched.begin(), touched.end());
-  touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
-  std::vector<uint8_t> orig(touched.size());
-  for (size_t k = 0; k < touched.size(); k++) orig[k] = c->grid_h[touched[k]];
+  std::vector<int32_t> touched;
+  std::vector<uint8_t> orig;
+  touched.reserve(n);
+  orig.reserve(n);
+  for (size_t k = 0; k < n; k++) {
+    const int32_t cell = xy[2 * k + 1] * w + xy[2 * k];
+    if (stamp[cell] != gen_t) {
+      stamp[cell] = gen_t;
+      touched.push_back(cell);
+      orig.push_back(c->grid_h[cell]);
+    }
+  }
   for (size_t k = 0; k < n; k++) c->grid_h[size_t(xy[2 * k + 1]) * w + xy[2 * k]] = occ[k] ? 1 : 0;
   std::vector<int32_t> changed;
   for (size_t k = 0; k < touched.size(); k++)
@@ -317,10 +396,14 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
     const int x = cell % w, y = cell / w;
     for (int dy = -1; dy <= 1; dy++)
       for (int dx = -1; dx <= 1; dx++)
-        if (inb(x + dx, y + dy)) window.push_back((y + dy) * w + (x + dx));
+        if (inb(x + dx, y + dy)) {
+          const int32_t q = (y + dy) * w + (x + dx);
+          if (stamp[q] != gen_w) {
+            stamp[q] = gen_w;
+            window.push_back(q);
+          }
+        }
   }
-  std::sort(window.begin(), window.end());
-  window.erase(std::unique(window.begin(), window.end()), window.end());
   std::vector<int32_t> wcells, dcells;
   std::vector<uint8_t> wflags;
   std::vector<int8_t> dsign;
@@ -351,26 +434,23 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
       c->member_h[cell] = member ? 1 : 0;
     }
   }
+#ifdef RL_EDIT_PROFILE
+  const double p1 = prof_now();
+  struct Pr {
+    double p0, p1;
+    ~Pr() { fprintf(stderr, "edit host %.1f us total %.1f us\n", p1 - p0, prof_now() - p0); }
+  } pr{p0, p1};
+#endif
   cudaStream_t st = c->stream;
   const size_t nw = wcells.size();
   const int nd = int(dcells.size());
-  const size_t rows = c->rows;
-  size_t scan_tmp = 0;
-  if (nd)
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, int(rows + 1), st);
-  const size_t cap = size_t(nd) * c->S * 3;  // a unit square spans at most 3 rows
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  // uploads wcells | wflags | dcells | dsign, staged through pinned memory so
-  // they go as one truly asynchronous copy
-  const size_t up_sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd)};
+  // uploads wcells | wflags | dcells | dsign | 32 zero bytes (the in-place
+  // path's control words), staged through pinned memory so they go as one
+  // truly asynchronous copy
+  const size_t up_sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd), 32};
   size_t up = 0;
   for (size_t b : up_sizes) up += al(b);
-  // one persistent workspace, carved in 256-byte aligned pieces
-  const size_t sizes[] = {up, 12 * rows, 8 * (rows + 1), 8 * (rows + 1), 4 * cap, cap, 8, scan_tmp};
-  size_t need = 0;
-  for (size_t b : sizes) need += al(b);
-  if (c->upd_ws.n < need) RL_TRY(c->upd_ws.alloc(need + need / 4));
   if (c->upd_host_n < up) {
     if (c->upd_host) cudaFreeHost(c->upd_host);
     c->upd_host = nullptr;
@@ -378,79 +458,559 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
     RL_CK(cudaMallocHost(&c->upd_host, up + up / 4));
     c->upd_host_n = up + up / 4;
   }
+  if (c->upd_up.n < up) RL_TRY(c->upd_up.alloc(up + up / 4));
+  size_t up_off[5];
+  {
+    uint8_t* hbuf = static_cast<uint8_t*>(c->upd_host);
+    const void* src[] = {wcells.data(), wflags.data(), dcells.data(), dsign.data(), nullptr};
+    size_t o = 0;
+    for (int k = 0; k < 5; k++) {
+      up_off[k] = o;
+      if (src[k] && up_sizes[k]) std::memcpy(hbuf + o, src[k], up_sizes[k]);
+      if (!src[k]) std::memset(hbuf + o, 0, up_sizes[k]);
+      o += al(up_sizes[k]);
+    }
+    RL_CK(cudaMemcpyAsync(c->upd_up.p, hbuf, up, cudaMemcpyHostToDevice, st));
+  }
+  const FlagEdits fe{reinterpret_cast<const int32_t*>(c->upd_up.p + up_off[0]),
+                     c->upd_up.p + up_off[1], int(nw)};
+  const EditBatch e{reinterpret_cast<const int32_t*>(c->upd_up.p + up_off[2]),
+                    reinterpret_cast<const int8_t*>(c->upd_up.p + up_off[3]), nd};
+  unsigned* ctl = reinterpret_cast<unsigned*>(c->upd_up.p + up_off[4]);
+  bool flags_done = false;
+  if (nd && c->gapped) {  // the touched rows only
+    bool applied = false;
+    RL_TRY(edits_in_place(c, fe, e, ctl, &applied));
+    if (applied) return finish(c, nullptr);
+    flags_done = true;  // a row needs the relayout; the flags are in place
+  }
+  if (!flags_done) {
+    k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(fe, c->w, c->wpr, c->flags.p, c->rowbits.p);
+    RL_CK(cudaGetLastError());
+  }
+  if (nd) RL_TRY(edits_relayout(c, e));
+  return finish(c, nullptr);
+}
+
+// All rows to fresh slots (slot_capacity) with the batch's deltas merged:
+// the first batch on a dense structure, and any batch a row outgrows its
+// slots in (or with more than kBucket records for one row).
+static int edits_relayout(rl_cddt* c, const EditBatch& e) {
+#ifdef RL_EDIT_PROFILE
+  fprintf(stderr, "relayout: %zu slots in use of %zu\n", size_t(c->zp_slots), size_t(c->zp.n));
+#endif
+  cudaStream_t st = c->stream;
+  const size_t rows = c->rows;
+  size_t scan_tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long*)nullptr,
+                                (unsigned long long*)nullptr, int(rows + 1), st);
+  const size_t cap = size_t(e.n) * c->S * 3;  // a unit square spans at most 3 rows
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  // one persistent workspace, carved in 256-byte aligned pieces
+  const size_t sizes[] = {12 * rows, 8 * (rows + 1), 8 * (rows + 1), 4 * cap, cap, 16, scan_tmp};
+  size_t need = 0;
+  for (size_t b : sizes) need += al(b);
+  if (c->upd_ws.n < need) RL_TRY(c->upd_ws.alloc(need + need / 4));
   uint8_t* cur = c->upd_ws.p;
   auto take = [&](size_t b) {
     uint8_t* p = cur;
     cur += al(b);
     return p;
   };
-  uint8_t* d_up = take(sizes[0]);
-  int32_t* add_cnt = reinterpret_cast<int32_t*>(take(sizes[1]));  // add | rem | cursor
+  int32_t* add_cnt = reinterpret_cast<int32_t*>(take(sizes[0]));  // add | rem | cursor
   int32_t* rem_cnt = add_cnt + rows;
   uint32_t* cursor = reinterpret_cast<uint32_t*>(rem_cnt + rows);
-  unsigned long long* packed = reinterpret_cast<unsigned long long*>(take(sizes[2]));
-  unsigned long long* packed_off = reinterpret_cast<unsigned long long*>(take(sizes[3]));
-  float* rec_v = reinterpret_cast<float*>(take(sizes[4]));
-  int8_t* rec_s = reinterpret_cast<int8_t*>(take(sizes[5]));
-  unsigned* d_unmatched = reinterpret_cast<unsigned*>(take(sizes[6]));
-  void* tmp = take(sizes[7]);
-  size_t up_off[4];
-  {
-    uint8_t* hbuf = static_cast<uint8_t*>(c->upd_host);
-    const void* src[] = {wcells.data(), wflags.data(), dcells.data(), dsign.data()};
-    size_t o = 0;
-    for (int k = 0; k < 4; k++) {
-      up_off[k] = o;
-      if (up_sizes[k]) std::memcpy(hbuf + o, src[k], up_sizes[k]);
-      o += al(up_sizes[k]);
-    }
-    RL_CK(cudaMemcpyAsync(d_up, hbuf, up, cudaMemcpyHostToDevice, st));
-  }
-  const int32_t* d_wcells = reinterpret_cast<const int32_t*>(d_up + up_off[0]);
-  const uint8_t* d_wflags = d_up + up_off[1];
-  const int32_t* d_dcells = reinterpret_cast<const int32_t*>(d_up + up_off[2]);
-  const int8_t* d_dsign = reinterpret_cast<const int8_t*>(d_up + up_off[3]);
-  k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(d_wcells, d_wflags, int(nw), c->flags.p);
-  RL_CK(cudaGetLastError());
-  RL_TRY(refresh_query_bits(c));
-  if (nd == 0) return finish(c, nullptr);
+  unsigned long long* packed = reinterpret_cast<unsigned long long*>(take(sizes[1]));
+  unsigned long long* packed_off = reinterpret_cast<unsigned long long*>(take(sizes[2]));
+  float* rec_v = reinterpret_cast<float*>(take(sizes[3]));
+  int8_t* rec_s = reinterpret_cast<int8_t*>(take(sizes[4]));
+  unsigned long long* ctl = reinterpret_cast<unsigned long long*>(take(sizes[5]));  // total | unmatched
+  void* tmp = take(sizes[6]);
 
-  // 3. per-row delta counts -> one scan (new offsets | delta buckets) -> records into buckets
+  // per-row delta counts -> one scan (new offsets | delta buckets) -> records into buckets
   RL_CK(cudaMemsetAsync(add_cnt, 0, 12 * rows, st));
-  RL_CK(cudaMemsetAsync(d_unmatched, 0, 4, st));
-  const int db = blocks_for(size_t(nd) * c->S, 256);
-  k_delta_count<<<db, 256, 0, st>>>(d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, add_cnt,
+  RL_CK(cudaMemsetAsync(ctl, 0, 16, st));
+  if (c->len_spare.n < rows) RL_TRY(c->len_spare.alloc(rows));
+  if (c->cap_spare.n < rows) RL_TRY(c->cap_spare.alloc(rows));
+  const int db = blocks_for(size_t(e.n) * c->S, 256);
+  k_delta_count<<<db, 256, 0, st>>>(e.cells, e.sign, e.n, c->d_slices.p, c->S, c->w, add_cnt,
                                     rem_cnt);
-  k_pack_len<<<blocks_for(rows + 1, 256), 256, 0, st>>>(c->row_off.p, add_cnt, rem_cnt, packed,
-                                                        rows);
+  k_pack_len<<<blocks_for(rows + 1, 256), 256, 0, st>>>(
+      c->row_off.p, c->gapped ? c->row_len.p : nullptr, add_cnt, rem_cnt, packed, c->len_spare.p,
+      c->cap_spare.p, ctl, rows);
   RL_CK(cub::DeviceScan::ExclusiveSum(tmp, scan_tmp, packed, packed_off, int(rows + 1), st));
-  k_delta_scatter<<<db, 256, 0, st>>>(d_dcells, d_dsign, nd, c->d_slices.p, c->S, w, packed_off,
+  k_delta_scatter<<<db, 256, 0, st>>>(e.cells, e.sign, e.n, c->d_slices.p, c->S, c->w, packed_off,
                                       cursor, rec_v, rec_s);
   RL_CK(cudaGetLastError());
-  // 4. merge into the spare buffers (the new offsets too), then swap
+  // merge into the spare buffers (the new offsets too), then swap
   if (c->off_spare.n < rows + 1) RL_TRY(c->off_spare.alloc(rows + 1));
-  const size_t zp_need = c->zero_points + cap;
-  if (c->zp_spare.n < zp_need) RL_TRY(c->zp_spare.alloc(zp_need + zp_need / 8));
+  const size_t pts = c->zero_points + cap;  // bound on the new point count
+  const size_t slots_ub = pts + pts / 8 + 4 * rows;
+  if (slots_ub >= (size_t(1) << 31)) {
+    set_error("cddt: %zu zero-point slots exceed the 31-bit CSR offset", slots_ub);
+    return RL_EINVAL;
+  }
+  // plus an append area for rows that outgrow their slots in later batches
+  // (RL_EDIT_APPEND_SLOTS overrides its size: a test hook for the exhausted-area path)
+  static const long long append_env = [] {
+    const char* v = std::getenv("RL_EDIT_APPEND_SLOTS");
+    return (v && *v) ? std::atoll(v) : -1ll;
+  }();
+  const size_t append = std::max(slots_ub / 4, size_t(1) << 20);
+  const size_t slots_buf = std::min(slots_ub + append, (size_t(1) << 31) - 1);
+  if (c->zp_spare.n < slots_buf) RL_TRY(c->zp_spare.alloc(slots_buf));
   k_merge_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(
-      c->row_off.p, c->zp.p, packed_off, c->off_spare.p, c->zp_spare.p, add_cnt, rem_cnt, rec_v,
-      rec_s, rows, d_unmatched, c->hints.p);
+      c->row_off.p, c->gapped ? c->row_len.p : nullptr, c->zp.p, packed_off, c->off_spare.p,
+      c->zp_spare.p, add_cnt, rem_cnt, rec_v, rec_s, rows,
+      reinterpret_cast<unsigned*>(ctl + 1), c->hints.p);
   RL_CK(cudaGetLastError());
-  uint32_t* total_miss = nullptr;  // pinned: {new zero-point total, missed removals}
-  RL_TRY(host_small(c, &total_miss));
-  RL_CK(cudaMemcpyAsync(&total_miss[0], packed_off + rows, 4, cudaMemcpyDeviceToHost, st));
-  RL_CK(cudaMemcpyAsync(&total_miss[1], d_unmatched, 4, cudaMemcpyDeviceToHost, st));
+  uint32_t* hs = nullptr;  // pinned: {slots, -, total points (u64), missed removals}
+  RL_TRY(host_small(c, &hs));
+  RL_CK(cudaMemcpyAsync(&hs[0], packed_off + rows, 4, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaMemcpyAsync(&hs[2], ctl, 12, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
-  if (total_miss[1]) {
+  uint64_t total = 0;
+  std::memcpy(&total, &hs[2], 8);
+  if (hs[4]) {
     set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)",
-              total_miss[1]);
+              hs[4]);
     return RL_ELOGIC;
   }
   std::swap(c->zp, c->zp_spare);
   std::swap(c->row_off, c->off_spare);  // the row records were rewritten by k_merge_rows
-  c->zero_points = total_miss[0];
-  return finish(c, nullptr);
+  std::swap(c->row_len, c->len_spare);
+  std::swap(c->row_cap, c->cap_spare);
+  c->zero_points = total;
+  c->zp_slots = hs[0];
+  c->slot_limit = append_env >= 0 ? std::min<uint64_t>(c->zp.n, c->zp_slots + append_env)
+                                  : c->zp.n;
+  c->gapped = true;
+  return RL_OK;
 }
 
+// ---- in place: only the touched rows ----
+//
+// Each touched row is merged where it lies when the merged row fits its slots
+// and the moved middle fits the warp's registers; otherwise it is rewritten
+// into fresh slots from the append area past zp_slots (and its record, offset
+// and capacity follow it). Only when the append area is exhausted, or a row
+// receives more than kBucket records, does the batch fall back to
+// edits_relayout — decided before anything is written.
+
+constexpr int kBucket = 32;               // delta records per row and batch (the warp merge's width)
+#ifndef RL_MID_REGS
+#define RL_MID_REGS 8
+#endif
+constexpr int kMidRegs = RL_MID_REGS;     // middle elements per lane held in registers
+constexpr int kMidMax = 32 * kMidRegs;    // longest middle merged in place
+constexpr int kMergeWarps = 4;            // warps per CTA of the plan and merge kernels
+
+// bkt layout (c->bkt): counts[rows] (zero between batches) | values[rows][kBucket] |
+// kinds[rows][kBucket] | planned positions[rows][kBucket] | touched-row list[rows] |
+// plan per list entry. The control words live in the batch's upload (zeroed).
+struct BucketView {
+  uint32_t* cnt;
+  float* val;
+  int8_t* sgn;     // +1 add, -1 remove; the plan sets 0 for a remove with no stored copy
+  uint32_t* pos;   // planned: a remove's claimed index, an add's insert position
+  uint32_t* list;
+  uint4* span;     // planned: {pmin, pend, net, new first slot or ~0u (in place)}
+  // ctl: list length, status (1: a bucket overflowed, 2: the append area is
+  // exhausted), missed removals, append slots reserved, net point change (i64)
+  unsigned* ctl;
+  long long* net;
+};
+
+// every (delta pixel, slice, row) record into its row's bucket; the first
+// record of a row lists the row. The leading blocks write the batch's flags.
+__global__ void k_flags_bucket(FlagEdits fe, int flag_blocks, int wpr, uint8_t* __restrict__ flags,
+                               uint2* __restrict__ bits, EditBatch e,
+                               const SliceParam* __restrict__ slices, int S, int w,
+                               BucketView b) {
+  if (int(blockIdx.x) < flag_blocks) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fe.n; i += flag_blocks * blockDim.x)
+      set_flag(fe, i, w, wpr, flags, bits);
+    return;
+  }
+  const int nb = gridDim.x - flag_blocks, bx = blockIdx.x - flag_blocks;
+  const int total = e.n * S;
+  for (int i = bx * blockDim.x + threadIdx.x; i < total; i += nb * blockDim.x) {
+    const int k = i / S, s = i % S;
+    const int cell = e.cells[k];
+    const SliceParam sp = slices[s];
+    int r0, r1;
+    float v;
+    pixel_rows_u(sp, cell % w, cell / w, r0, r1, v);
+    for (int r = r0; r <= r1; r++) {
+      const uint32_t g = sp.row_base + uint32_t(r);
+      const uint32_t slot = atomicAdd(&b.cnt[g], 1u);
+      if (slot == 0) b.list[atomicAdd(&b.ctl[0], 1u)] = g;
+      if (slot < kBucket) {
+        b.val[size_t(g) * kBucket + slot] = v;
+        b.sgn[size_t(g) * kBucket + slot] = e.sign[k];
+      } else {
+        atomicOr(&b.ctl[1], 1u);
+      }
+    }
+  }
+}
+
+// Where a row's bucket lands (the order-free merge of k_merge_rows, per
+// lane = per record): a remove claims old copy lower_bound(v) + its rank among
+// the equal removes; an add goes in at upper_bound(v). Old elements before
+// the first claimed/insert position keep their index, those from `pend` on
+// all shift by `net`; only the middle [pmin, pend) moves irregularly.
+struct MergePlan {
+  float dv;
+  bool add, rem;       // rem: a remove that found its copy
+  uint32_t pos;        // rem: the claimed index; add: the insert position
+  unsigned add_mask, rem_mask;
+  uint32_t pmin, pend;
+  int net;
+};
+
+// new index of old element i (value x) of the middle; false: removed
+__device__ __forceinline__ bool middle_dest(const MergePlan& p, uint32_t i, float x,
+                                            uint32_t* dst) {
+  bool removed = false;
+  unsigned rb = 0, adds_lt = 0;
+  const unsigned any = p.add_mask | p.rem_mask;
+  for (unsigned l = 0; l < 32; l++) {
+    if (!((any >> l) & 1u)) continue;  // warp-uniform
+    const uint32_t pl = __shfl_sync(0xffffffffu, p.pos, l);
+    const float dl = __shfl_sync(0xffffffffu, p.dv, l);
+    if ((p.rem_mask >> l) & 1u) {
+      removed |= pl == i;
+      rb += pl < i ? 1u : 0u;
+    } else {
+      adds_lt += dl < x ? 1u : 0u;
+    }
+  }
+  *dst = i - rb + adds_lt;
+  return !removed;
+}
+
+// new index of this lane's add: after the kept copies <= dv, the smaller adds
+// and the equal adds of lower lanes (call from every lane: it shuffles)
+__device__ __forceinline__ uint32_t add_dest(const MergePlan& p) {
+  const unsigned lane = threadIdx.x & 31;
+  unsigned rem_lt = 0, adds_before = 0;
+  const unsigned any = p.add_mask | p.rem_mask;
+  for (unsigned l = 0; l < 32; l++) {
+    if (!((any >> l) & 1u)) continue;
+    const uint32_t pl = __shfl_sync(0xffffffffu, p.pos, l);
+    const float dl = __shfl_sync(0xffffffffu, p.dv, l);
+    if ((p.rem_mask >> l) & 1u)
+      rem_lt += pl < p.pos ? 1u : 0u;
+    else
+      adds_before += (dl < p.dv || (dl == p.dv && l < lane)) ? 1u : 0u;
+  }
+  return p.pos - rem_lt + adds_before;
+}
+
+// Per touched row (one warp): the record positions, the middle, and whether
+// the row merges in place or into fresh slots from the append area. All
+// reservations are made here, so an exhausted append area is known before
+// anything is written.
+__global__ void __launch_bounds__(32 * kMergeWarps) k_bucket_plan(
+    BucketView b, const uint32_t* __restrict__ off, const uint32_t* __restrict__ cap,
+    const uint32_t* __restrict__ len, const float* __restrict__ zp, uint32_t append_base,
+    uint32_t slots_total) {
+  const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
+  const unsigned m = b.ctl[0];
+  if (b.ctl[1]) return;  // a bucket overflowed: relayout
+  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned j = warp; j < m; j += nwarps) {
+    const uint32_t g = b.list[j];
+    const unsigned nd = b.cnt[g];
+    const uint32_t n = len[g];
+    const float* __restrict__ row = zp + off[g];
+    const size_t r0 = size_t(g) * kBucket;
+    const bool has = lane < nd;
+    const float dv = has ? b.val[r0 + lane] : 0.f;
+    const bool add = has && b.sgn[r0 + lane] > 0;
+    bool rem = has && !add;
+    const unsigned rem_all = __ballot_sync(0xffffffffu, rem);
+    const unsigned same = __match_any_sync(0xffffffffu, __float_as_uint(dv)) & rem_all;
+    uint32_t pos = 0;
+    if (rem) {
+      const uint32_t q = row_bound(row, n, dv, false) + __popc(same & lt);
+      if (q < n && row[q] == dv) {
+        pos = q;
+      } else {
+        rem = false;
+        b.sgn[r0 + lane] = 0;  // missed: reported by the merge
+      }
+    }
+    if (add) pos = row_bound(row, n, dv, true);
+    if (has) b.pos[r0 + lane] = pos;
+    const int net = __popc(__ballot_sync(0xffffffffu, add)) - __popc(__ballot_sync(0xffffffffu, rem));
+    uint32_t lo = (add || rem) ? pos : 0xffffffffu;
+    uint32_t hi = rem ? pos + 1 : (add ? pos : 0u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const uint32_t pmin = lo == 0xffffffffu ? n : lo, pend = hi < pmin ? pmin : hi;
+    if (lane == 0) {
+      const uint32_t nn = uint32_t(int(n) + net);
+      uint32_t target = ~0u;
+      if (nn > cap[g] || pend - pmin > uint32_t(kMidMax)) {
+        const uint32_t need = slot_capacity(nn);
+        const uint32_t at = atomicAdd(&b.ctl[3], need);
+        if (uint64_t(append_base) + at + need > slots_total)
+          atomicOr(&b.ctl[1], 2u);
+        else
+          target = append_base + at;
+      }
+      b.span[j] = make_uint4(pmin, pend, uint32_t(net), target);
+    }
+  }
+}
+
+// One warp per touched row: the planned merge, in place or into its fresh
+// slots; then the row's record, length (offset and capacity when it moved).
+// With a status flag set nothing is written (the batch goes to
+// edits_relayout); the counts are zeroed either way.
+__global__ void __launch_bounds__(32 * kMergeWarps) k_merge_touched(
+    BucketView b, uint32_t* __restrict__ off, uint32_t* __restrict__ cap,
+    uint32_t* __restrict__ len, float* __restrict__ zp, float* __restrict__ hints) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned m = b.ctl[0];
+  const bool skip = b.ctl[1] != 0;
+  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  long long net = 0;
+  unsigned missed = 0;
+  for (unsigned j = warp; j < m; j += nwarps) {
+    const uint32_t g = b.list[j];
+    if (skip) {
+      if (lane == 0) b.cnt[g] = 0;
+      continue;
+    }
+    const unsigned nd = b.cnt[g];
+    const uint32_t lo = off[g], n = len[g];
+    const float* row = zp + lo;
+    const uint4 sp = b.span[j];
+    const size_t r0 = size_t(g) * kBucket;
+    MergePlan p;
+    const bool has = lane < nd;
+    const int8_t kind = has ? b.sgn[r0 + lane] : int8_t(0);
+    p.dv = has ? b.val[r0 + lane] : 0.f;
+    p.pos = has ? b.pos[r0 + lane] : 0u;
+    p.add = kind > 0;
+    p.rem = kind < 0;
+    missed += (has && kind == 0) ? 1u : 0u;
+    p.add_mask = __ballot_sync(0xffffffffu, p.add);
+    p.rem_mask = __ballot_sync(0xffffffffu, p.rem);
+    p.pmin = sp.x;
+    p.pend = sp.y;
+    p.net = int(sp.z);
+    const uint32_t target = sp.w;
+    const uint32_t nn = uint32_t(int(n) + p.net);
+    if (target != ~0u) {  // fresh slots: no overlap, straight copies around the middle
+      float* dst = zp + target;
+      for (uint32_t i = lane; i < p.pmin; i += 32) dst[i] = row[i];
+      for (uint32_t i = p.pend + lane; i < n; i += 32) dst[int(i) + p.net] = row[i];
+      for (uint32_t base = p.pmin; base < p.pend; base += 32) {  // warp-uniform trips
+        const uint32_t i = base + lane;
+        const float x = i < p.pend ? row[i] : 0.f;
+        uint32_t d;
+        const bool keep = middle_dest(p, i, x, &d);
+        if (i < p.pend && keep) dst[d] = x;
+      }
+      const uint32_t ad = add_dest(p);  // every lane: add_dest shuffles
+      if (p.add) dst[ad] = p.dv;
+    } else {
+      float* dst = zp + lo;
+      // the middle into registers before anything moves
+      float mid[kMidRegs];
+#pragma unroll
+      for (int k = 0; k < kMidRegs; k++) {
+        const uint32_t i = p.pmin + lane + 32u * k;
+        mid[k] = i < p.pend ? row[i] : 0.f;
+      }
+      // the tail [pend, n) shifts by net, kTailGroup chunks of 32 per round
+      // trip: groups from the far end when it grows, from the near end when it
+      // shrinks (each group is read before it is written)
+      if (p.net != 0 && p.pend < n) {
+        constexpr uint32_t kG = 32u * kMidRegs;
+        const uint32_t span = n - p.pend, groups = (span + kG - 1) / kG;
+        for (uint32_t q = 0; q < groups; q++) {
+          const uint32_t g0 = p.pend + (p.net > 0 ? (groups - 1 - q) : q) * kG;
+          float t[kMidRegs];
+#pragma unroll
+          for (int k = 0; k < kMidRegs; k++) {
+            const uint32_t i = g0 + lane + 32u * k;
+            t[k] = i < n ? row[i] : 0.f;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < kMidRegs; k++) {
+            const uint32_t i = g0 + lane + 32u * k;
+            if (i < n) dst[int(i) + p.net] = t[k];
+          }
+          __syncwarp();
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < kMidRegs; k++) {
+        const uint32_t i = p.pmin + lane + 32u * k;
+        if (p.pmin + 32u * k >= p.pend) break;  // warp-uniform
+        uint32_t d;
+        const bool keep = middle_dest(p, i, mid[k], &d);
+        if (i < p.pend && keep) dst[d] = mid[k];
+      }
+      const uint32_t ad = add_dest(p);  // every lane: add_dest shuffles
+      if (p.add) dst[ad] = p.dv;
+    }
+    __syncwarp();  // the warp's stores of the new row are visible to lane 0
+    if (lane == 0) {
+      const uint32_t at = target != ~0u ? target : lo;
+      write_row_record(hints, g, at, zp + at, nn);
+      len[g] = nn;
+      if (target != ~0u) {
+        off[g] = target;
+        cap[g] = slot_capacity(nn);
+      }
+      b.cnt[g] = 0;
+      net += (long long)nn - (long long)n;
+    }
+  }
+  if (lane == 0 && net)
+    atomicAdd(reinterpret_cast<unsigned long long*>(b.net), static_cast<unsigned long long>(net));
+  if (missed) atomicAdd(&b.ctl[2], missed);
+}
+
+static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, unsigned* ctl,
+                          bool* applied) {
+  *applied = false;
+  cudaStream_t st = c->stream;
+  const size_t rows = c->rows;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t sizes[] = {4 * rows, 4 * rows * kBucket, rows * kBucket, 4 * rows * kBucket,
+                          4 * rows, 16 * rows};
+  size_t need = 0;
+  for (size_t s : sizes) need += al(s);
+  if (c->bkt.n < need) {
+    RL_TRY(c->bkt.alloc(need));
+    RL_CK(cudaMemsetAsync(c->bkt.p, 0, al(sizes[0]), st));  // counts start (and stay) zero
+  }
+  uint8_t* cur = c->bkt.p;
+  auto take = [&](size_t s) {
+    uint8_t* p = cur;
+    cur += al(s);
+    return p;
+  };
+  BucketView b;
+  b.cnt = reinterpret_cast<uint32_t*>(take(sizes[0]));
+  b.val = reinterpret_cast<float*>(take(sizes[1]));
+  b.sgn = reinterpret_cast<int8_t*>(take(sizes[2]));
+  b.pos = reinterpret_cast<uint32_t*>(take(sizes[3]));
+  b.list = reinterpret_cast<uint32_t*>(take(sizes[4]));
+  b.span = reinterpret_cast<uint4*>(take(sizes[5]));
+  b.ctl = ctl;
+  b.net = reinterpret_cast<long long*>(ctl + 4);
+  const int fb = blocks_for(size_t(fe.n), 256, 2);
+  const int bb = blocks_for(size_t(e.n) * c->S, 256);
+  k_flags_bucket<<<fb + bb, 256, 0, st>>>(fe, fb, c->wpr, c->flags.p, c->rowbits.p, e,
+                                          c->d_slices.p, c->S, c->w, b);
+  // latency-bound warps (a chain of dependent loads per row): fill the GPU
+  static const int plan_ctas = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_plan, 32 * kMergeWarps, 0);
+    return sm_count() * std::max(per_sm, 1);
+  }();
+  static const int merge_ctas = [] {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_touched, 32 * kMergeWarps, 0);
+    return sm_count() * std::max(per_sm, 1);
+  }();
+  k_bucket_plan<<<plan_ctas, 32 * kMergeWarps, 0, st>>>(b, c->row_off.p, c->row_cap.p, c->row_len.p,
+                                                 c->zp.p, uint32_t(c->zp_slots),
+                                                 uint32_t(c->slot_limit));
+  k_merge_touched<<<merge_ctas, 32 * kMergeWarps, 0, st>>>(b, c->row_off.p, c->row_cap.p, c->row_len.p,
+                                                   c->zp.p, c->hints.p);
+  RL_CK(cudaGetLastError());
+  uint32_t* hs = nullptr;
+  RL_TRY(host_small(c, &hs));
+  RL_CK(cudaMemcpyAsync(hs, ctl, 32, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaStreamSynchronize(st));
+#ifdef RL_EDIT_PROFILE
+  fprintf(stderr, "in-place status %u rows %u appended %u of %zu free\n", hs[1], hs[0], hs[3],
+          size_t(c->zp.n - c->zp_slots));
+#endif
+  if (hs[1]) return RL_OK;  // nothing written: relayout
+  if (hs[2]) {
+    set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)",
+              hs[2]);
+    return RL_ELOGIC;
+  }
+  long long net = 0;
+  std::memcpy(&net, hs + 4, 8);
+  c->zero_points = uint64_t((long long)c->zero_points + net);
+  c->zp_slots += hs[3];
+  *applied = true;
+  return RL_OK;
+}
+
+// Slack rows back to dense CSR (before prune): one scan of the row lengths,
+// one warp per row copying it down.
+__global__ void k_len_wide(const uint32_t* __restrict__ len, uint32_t* __restrict__ out,
+                           size_t rows) {
+  for (size_t g = blockIdx.x * size_t(blockDim.x) + threadIdx.x; g <= rows;
+       g += size_t(gridDim.x) * blockDim.x)
+    out[g] = g < rows ? len[g] : 0u;
+}
+__global__ void k_copy_rows(const uint32_t* __restrict__ off, const uint32_t* __restrict__ len,
+                            const float* __restrict__ zp, const uint32_t* __restrict__ noff,
+                            float* __restrict__ nzp, size_t rows) {
+  const unsigned lane = threadIdx.x & 31;
+  const size_t warp = (blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5;
+  const size_t nwarps = (size_t(gridDim.x) * blockDim.x) >> 5;
+  for (size_t g = warp; g < rows; g += nwarps)
+    for (uint32_t i = lane; i < len[g]; i += 32) nzp[noff[g] + i] = zp[off[g] + i];
+}
+
+}  // namespace rl
+
+namespace rl {
+int densify_rows(rl_cddt* c) {
+  if (!c->gapped) return RL_OK;
+  cudaStream_t st = c->stream;
+  const size_t rows = c->rows;
+  DevBuf<uint32_t> wide, noff;
+  DevBuf<float> nzp;
+  RL_TRY(wide.alloc(rows + 1));
+  RL_TRY(noff.alloc(rows + 1));
+  RL_TRY(nzp.alloc(c->zero_points));
+  k_len_wide<<<blocks_for(rows + 1, 256), 256, 0, st>>>(c->row_len.p, wide.p, rows);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, wide.p, noff.p, int(rows + 1), st);
+  DevBuf<uint8_t> tmp;
+  RL_TRY(tmp.alloc(tmp_bytes));
+  RL_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, wide.p, noff.p, int(rows + 1), st));
+  k_copy_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(c->row_off.p, c->row_len.p,
+                                                               c->zp.p, noff.p, nzp.p, rows);
+  RL_CK(cudaGetLastError());
+  RL_CK(cudaStreamSynchronize(st));
+  c->zp = std::move(nzp);
+  c->row_off = std::move(noff);
+  c->row_len.release();
+  c->len_spare.release();
+  c->row_cap.release();
+  c->cap_spare.release();
+  c->zp_spare.release();
+  c->off_spare.release();
+  c->zp_slots = c->zero_points;
+  c->gapped = false;
+  RL_TRY(refresh_row_hints(c));
+  RL_CK(cudaStreamSynchronize(st));
+  return RL_OK;
+}
 }  // namespace rl
 
 using namespace rl;
