@@ -577,6 +577,27 @@ int create_handle(int32_t device, rl_cddt** out, rl_cddt** keep) {
 
 using namespace rl;
 
+namespace rl {
+// The host grid/membership mirrors after edits replayed on the device: one
+// download of the flags (occupancy and membership bits).
+int refresh_mirrors(const rl_cddt* cc) {
+  rl_cddt* c = const_cast<rl_cddt*>(cc);
+  if (!c->mirror_stale) return RL_OK;
+  const size_t wh = size_t(c->w) * c->h;
+  std::vector<uint8_t> fl(wh);
+  RL_CK(cudaMemcpyAsync(fl.data(), c->flags.p, wh, cudaMemcpyDeviceToHost, c->stream));
+  RL_CK(cudaStreamSynchronize(c->stream));
+  c->grid_h.resize(wh);
+  c->member_h.resize(wh);
+  for (size_t i = 0; i < wh; i++) {
+    c->grid_h[i] = (fl[i] & kOcc) ? 1 : 0;
+    c->member_h[i] = (fl[i] & kMember) ? 1 : 0;
+  }
+  c->mirror_stale = false;
+  return RL_OK;
+}
+}  // namespace rl
+
 extern "C" {
 
 const char* rl_last_error(void) { return g_err.c_str(); }
@@ -651,6 +672,7 @@ int rl_cddt_create(const uint8_t* grid, int32_t width, int32_t height, double re
   return RL_OK;
 }
 
+
 int rl_cddt_destroy(rl_cddt* c) {
   if (!c) return RL_OK;
   {
@@ -677,6 +699,8 @@ int rl_cddt_destroy(rl_cddt* c) {
     c->row_cap.release();
     c->cap_spare.release();
     c->bkt.release();
+    c->estamp.release();
+    c->wstamp.release();
     c->pf_ctl.release();
     if (c->pf_host) cudaFreeHost(c->pf_host);
     if (c->host_small) cudaFreeHost(c->host_small);
@@ -729,6 +753,7 @@ int rl_cddt_export(const rl_cddt* c, uint32_t* slice_row_base, uint64_t* row_off
   if (!c) return RL_EINVAL;
   DeviceGuard guard(c->dev);
   RL_CK(cudaStreamSynchronize(c->stream));
+  if (membership || grid) RL_TRY(refresh_mirrors(c));
   if (slice_row_base) {
     for (int s = 0; s < c->S; s++) slice_row_base[s] = c->slices[s].row_base;
     slice_row_base[c->S] = uint32_t(c->rows);

@@ -116,8 +116,7 @@ struct rl_cddt {
 
   std::vector<uint8_t> grid_h;    // host mirror: occupancy
   std::vector<uint8_t> member_h;  // host mirror: membership
-  std::vector<uint32_t> stamp;    // incremental edits: per-cell generation stamps (dedup)
-  uint32_t stamp_gen = 0;
+  bool mirror_stale = false;      // edits ran on the device since the mirrors were filled
 
   rl::DevBuf<uint8_t> flags;        // w*h
   rl::DevBuf<uint2> rowbits;        // row-major occupancy/clear bits for queries
@@ -157,6 +156,9 @@ struct rl_cddt {
   rl::DevBuf<uint32_t> len_spare;   // incremental edits: double buffers for row_len / row_cap
   rl::DevBuf<uint32_t> cap_spare;
   rl::DevBuf<uint8_t> bkt;          // incremental edits: per-row delta buckets (zeroed counts)
+  rl::DevBuf<uint32_t> estamp;      // incremental edits: per-cell (generation, edit) stamps
+  rl::DevBuf<uint32_t> wstamp;      // incremental edits: per-cell dilation stamps
+  uint32_t edit_gen = 0;
 
   rl::CddtView view() const {
     rl::CddtView v;
@@ -191,6 +193,7 @@ int finish(const rl_cddt* c, void* s);  // sync when the caller passed no stream
 int refresh_query_bits(rl_cddt* c);     // rebuild the query occupancy bits from flags
 int refresh_row_hints(rl_cddt* c);      // rebuild the row search hints from row_off / zp
 int densify_rows(rl_cddt* c);           // slack rows back to dense CSR (rl_update.cu)
+int refresh_mirrors(const rl_cddt* c);  // host grid/membership mirrors from the device flags
 // stream-ordered scratch from the library's own per-device pool (rl_cddt.cu)
 int scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 int scratch_free(void* p, cudaStream_t st);

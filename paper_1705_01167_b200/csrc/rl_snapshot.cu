@@ -67,6 +67,10 @@ int rl_cddt_serialize(const rl_cddt* c, uint8_t* buf, size_t cap, size_t* size) 
   std::vector<float> zp(c->zero_points);
   std::vector<uint64_t> off(c->rows + 1);
   RL_TRY(rl_cddt_export(c, nullptr, off.data(), zp.data(), nullptr, nullptr));
+  {
+    DeviceGuard guard(c->dev);
+    RL_TRY(refresh_mirrors(c));  // the grid and membership bitmaps below
+  }
   std::vector<uint8_t> out;
   out.reserve(64 + 2 * ((wh + 7) / 8) + 4 * c->zero_points + 4 * c->rows + 4 * c->S);
   out.push_back('C');

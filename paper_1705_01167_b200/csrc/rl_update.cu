@@ -300,155 +300,150 @@ __global__ void k_merge_rows(const uint32_t* __restrict__ old_off,
   }
 }
 
-// The recomputed flags of the batch's dilation, and the same bits in the
-// query bitmaps (rowbits: per 32-cell word {occupied, clear}) — only the
-// words of the changed cells, by atomic bit updates.
-struct FlagEdits {
-  const int32_t* cells;
-  const uint8_t* f;
-  int n;
-};
-__device__ __forceinline__ void set_flag(const FlagEdits& fe, int i, int w, int wpr,
-                                         uint8_t* __restrict__ flags, uint2* __restrict__ bits) {
-  const int32_t cell = fe.cells[i];
-  const uint8_t f = fe.f[i];
-  flags[cell] = f;
-  const int x = cell % w, y = cell / w;
-  unsigned* word = reinterpret_cast<unsigned*>(bits + size_t(y) * wpr + (x >> 5));
-  const unsigned bit = 1u << (x & 31);
-  if (f & kOcc)
-    atomicOr(word, bit);
-  else
-    atomicAnd(word, ~bit);
-  if (f & kClear)
-    atomicOr(word + 1, bit);
-  else
-    atomicAnd(word + 1, ~bit);
-}
-__global__ void k_set_flags(FlagEdits fe, int w, int wpr, uint8_t* __restrict__ flags,
-                            uint2* __restrict__ bits) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fe.n; i += gridDim.x * blockDim.x)
-    set_flag(fe, i, w, wpr, flags, bits);
-}
-
 static int blocks_for(size_t work, int threads, int cap_per_sm = 16) {
   size_t b = (work + threads - 1) / threads;
   size_t cap = size_t(sm_count()) * cap_per_sm;
   return int(std::max<size_t>(1, std::min(b, cap)));
 }
 
-// The batch's membership deltas on the device: pixels and +1 (joins) / -1 (leaves).
-struct EditBatch {
-  const int32_t* cells;
-  const int8_t* sign;
-  int n;
-};
-static int edits_relayout(rl_cddt* c, const EditBatch& e);
-static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, unsigned* ctl,
-                          bool* applied);
+// ---- the batch replayed on the device ----
+//
+// Cddt::set_occupancy applied cell by cell in order (cddt.cpp:332-377) ends
+// in the state of a fresh build of the final grid (the reference's invariant,
+// proj/tests/test_cddt.cpp:578-604), so a batch reduces to: the final
+// occupancy of every touched cell (the last edit of a cell wins), the flags
+// of the changed cells' 3x3 dilation recomputed from it, and the membership
+// flips there (the delta pixels, +1 joins / -1 leaves). Three small kernels;
+// per-cell generation stamps pick the last edit and deduplicate the dilation
+// without clearing anything between batches.
 
-// Apply edits [0, n) (already validated) to the structure.
-#ifdef RL_EDIT_PROFILE
-#include <chrono>
-static double prof_now() {
-  return std::chrono::duration<double, std::micro>(
-             std::chrono::steady_clock::now().time_since_epoch()).count();
+// control words of a batch (zeroed by its upload)
+enum : int {
+  kCtlRows = 0,      // touched-row list length (in place)
+  kCtlStatus = 1,    // 1: a bucket overflowed, 2: the append area is exhausted
+  kCtlMissed = 2,    // removals that found no stored point
+  kCtlAppend = 3,    // append slots reserved
+  kCtlNet = 4,       // net point change (i64, words 4-5)
+  kCtlChanged = 6,   // cells whose occupancy changed
+  kCtlDeltas = 7,    // delta pixels
+  kCtlWords = 8
+};
+constexpr int kEditBits = 20;  // edit index bits of a stamp (batches go in chunks of 2^20)
+
+// every edit stamps its cell with (generation, index): the largest index wins
+__global__ void k_replay_stamp(const int32_t* __restrict__ xy, int n, int w,
+                               uint32_t* __restrict__ stamp, uint32_t gen) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    atomicMax(&stamp[size_t(xy[2 * k + 1]) * w + xy[2 * k]], (gen << kEditBits) | uint32_t(k));
 }
-#endif
-static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n) {
-#ifdef RL_EDIT_PROFILE
-  const double p0 = prof_now();
-#endif
-  const int w = c->w, h = c->h;
-  auto at = [&](int x, int y) { return c->grid_h[size_t(y) * w + x] != 0; };
-  auto inb = [&](int x, int y) { return x >= 0 && y >= 0 && x < w && y < h; };
-  // cells are deduplicated with generation stamps (no sort: a batch touches
-  // a few thousand cells, and sorting them cost more than the GPU work)
-  if (c->stamp.size() != size_t(w) * h || c->stamp_gen > 0xfffffff0u) {
-    c->stamp.assign(size_t(w) * h, 0u);
-    c->stamp_gen = 0;
+
+// the last edit of each cell sets its occupancy; changed cells are listed
+__global__ void k_replay_apply(const int32_t* __restrict__ xy, const uint8_t* __restrict__ occ,
+                               int n, int w, const uint32_t* __restrict__ stamp, uint32_t gen,
+                               uint8_t* __restrict__ flags, int32_t* __restrict__ changed,
+                               unsigned* __restrict__ ctl) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const size_t cell = size_t(xy[2 * k + 1]) * w + xy[2 * k];
+    if (stamp[cell] != ((gen << kEditBits) | uint32_t(k))) continue;  // a later edit wins
+    const uint8_t f = flags[cell];
+    const bool o = occ[k] != 0;
+    if (o == ((f & kOcc) != 0)) continue;
+    flags[cell] = o ? uint8_t(f | kOcc) : uint8_t(f & ~kOcc);
+    changed[atomicAdd(&ctl[kCtlChanged], 1u)] = int32_t(cell);
   }
-  const uint32_t gen_t = ++c->stamp_gen, gen_w = ++c->stamp_gen;
-  uint32_t* stamp = c->stamp.data();
-  // 1. the touched cells' original states, then replay in order (last writer
-  //    wins); changed = touched cells whose final state differs
-  std::vector<int32_t> touched;
-  std::vector<uint8_t> orig;
-  touched.reserve(n);
-  orig.reserve(n);
-  for (size_t k = 0; k < n; k++) {
-    const int32_t cell = xy[2 * k + 1] * w + xy[2 * k];
-    if (stamp[cell] != gen_t) {
-      stamp[cell] = gen_t;
-      touched.push_back(cell);
-      orig.push_back(c->grid_h[cell]);
-    }
-  }
-  for (size_t k = 0; k < n; k++) c->grid_h[size_t(xy[2 * k + 1]) * w + xy[2 * k]] = occ[k] ? 1 : 0;
-  std::vector<int32_t> changed;
-  for (size_t k = 0; k < touched.size(); k++)
-    if (orig[k] != c->grid_h[touched[k]]) changed.push_back(touched[k]);
-  if (changed.empty()) return RL_OK;
-  // 2. flags in the dilation; membership deltas
-  std::vector<int32_t> window;
-  window.reserve(changed.size() * 9);
-  for (int32_t cell : changed) {
-    const int x = cell % w, y = cell / w;
-    for (int dy = -1; dy <= 1; dy++)
-      for (int dx = -1; dx <= 1; dx++)
-        if (inb(x + dx, y + dy)) {
-          const int32_t q = (y + dy) * w + (x + dx);
-          if (stamp[q] != gen_w) {
-            stamp[q] = gen_w;
-            window.push_back(q);
-          }
-        }
-  }
-  std::vector<int32_t> wcells, dcells;
-  std::vector<uint8_t> wflags;
-  std::vector<int8_t> dsign;
-  wcells.reserve(window.size());
-  for (const int32_t cell : window) {
-    const int x = cell % w, y = cell / w;
-    const bool o = at(x, y);
+}
+
+// The 3x3 dilation of the changed cells (each cell once: the first thread to
+// raise its stamp to this generation): occupancy / clear / membership flags
+// from the final occupancy (is_edge_cell, grid.cpp:110-119; clear_around,
+// cddt.cpp:173-180), the same bits in the query bitmaps, and the membership
+// flips as delta pixels. Only clear/member bits are written here, so the
+// occupancy bits other threads read are final.
+__global__ void k_replay_flags(const int32_t* __restrict__ changed, int w, int h, int wpr,
+                               uint32_t* __restrict__ wstamp, uint32_t gen,
+                               uint8_t* __restrict__ flags, uint2* __restrict__ bits,
+                               int32_t* __restrict__ dcells, int8_t* __restrict__ dsign,
+                               unsigned* __restrict__ ctl) {
+  const unsigned m = ctl[kCtlChanged] * 9u;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int32_t c0 = changed[i / 9];
+    const int x = c0 % w + int(i % 9) % 3 - 1, y = c0 / w + int(i % 9) / 3 - 1;
+    if (x < 0 || y < 0 || x >= w || y >= h) continue;
+    const size_t q = size_t(y) * w + x;
+    if (atomicMax(&wstamp[q], gen) >= gen) continue;  // another thread has this cell
+    const uint8_t old = flags[q];
+    const bool o = (old & kOcc) != 0;
     bool any_occ = false, any_free = false;
     for (int dy = -1; dy <= 1; dy++)
       for (int dx = -1; dx <= 1; dx++) {
         if (dx == 0 && dy == 0) continue;
         const int nx = x + dx, ny = y + dy;
-        if (!inb(nx, ny) || !at(nx, ny))
+        if (nx < 0 || ny < 0 || nx >= w || ny >= h || !(flags[size_t(ny) * w + nx] & kOcc))
           any_free = true;
         else
           any_occ = true;
       }
-    const bool member = o && any_free;  // is_edge_cell (grid.cpp:110-119)
-    uint8_t f = 0;
-    if (o) f |= kOcc;
-    if (!o && !any_occ) f |= kClear;  // clear_around (cddt.cpp:173-180)
+    const bool member = o && any_free;
+    const bool clear = !o && !any_occ;
+    uint8_t f = o ? kOcc : 0;
+    if (clear) f |= kClear;
     if (member) f |= kMember;
-    wcells.push_back(cell);
-    wflags.push_back(f);
-    if (member != (c->member_h[cell] != 0)) {
-      dcells.push_back(cell);
-      dsign.push_back(member ? 1 : -1);
-      c->member_h[cell] = member ? 1 : 0;
+    flags[q] = f;
+    unsigned* word = reinterpret_cast<unsigned*>(bits + size_t(y) * wpr + (x >> 5));
+    const unsigned bit = 1u << (x & 31);
+    if (o)
+      atomicOr(word, bit);
+    else
+      atomicAnd(word, ~bit);
+    if (clear)
+      atomicOr(word + 1, bit);
+    else
+      atomicAnd(word + 1, ~bit);
+    if (member != ((old & kMember) != 0)) {
+      const unsigned d = atomicAdd(&ctl[kCtlDeltas], 1u);
+      dcells[d] = int32_t(q);
+      dsign[d] = member ? int8_t(1) : int8_t(-1);
     }
   }
-#ifdef RL_EDIT_PROFILE
-  const double p1 = prof_now();
-  struct Pr {
-    double p0, p1;
-    ~Pr() { fprintf(stderr, "edit host %.1f us total %.1f us\n", p1 - p0, prof_now() - p0); }
-  } pr{p0, p1};
-#endif
+}
+
+// The batch's membership deltas on the device: pixels and +1 (joins) / -1
+// (leaves); *n_dev their count (the host learns it as `n` only when the
+// relayout needs it).
+struct EditBatch {
+  const int32_t* cells;
+  const int8_t* sign;
+  const unsigned* n_dev;
+  int n_bound;  // upper bound on the count (launch sizing)
+  int n;        // the count, when known on the host
+};
+static int edits_relayout(rl_cddt* c, const EditBatch& e);
+static int edits_in_place(rl_cddt* c, const EditBatch& e, unsigned* ctl, bool* applied);
+
+// Apply edits [0, n) (already validated) to the structure, in order: chunks
+// of 2^20 edits (the stamp's index field), each replayed on the device.
+static int apply_chunk(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n);
+static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n) {
+  constexpr size_t kChunk = size_t(1) << kEditBits;
+  for (size_t off = 0; off < n; off += kChunk)
+    RL_TRY(apply_chunk(c, xy + 2 * off, occ + off, std::min(kChunk, n - off)));
+  return RL_OK;
+}
+
+static int apply_chunk(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t n) {
   cudaStream_t st = c->stream;
-  const size_t nw = wcells.size();
-  const int nd = int(dcells.size());
+  const size_t wh = size_t(c->w) * c->h;
+  if (c->estamp.n != wh || c->wstamp.n != wh || c->edit_gen + 1 >= (1u << (32 - kEditBits))) {
+    if (c->estamp.n != wh) RL_TRY(c->estamp.alloc(wh));
+    if (c->wstamp.n != wh) RL_TRY(c->wstamp.alloc(wh));
+    RL_CK(cudaMemsetAsync(c->estamp.p, 0, 4 * wh, st));
+    RL_CK(cudaMemsetAsync(c->wstamp.p, 0, 4 * wh, st));
+    c->edit_gen = 0;
+  }
+  const uint32_t gen = ++c->edit_gen;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  // uploads wcells | wflags | dcells | dsign | 32 zero bytes (the in-place
-  // path's control words), staged through pinned memory so they go as one
-  // truly asynchronous copy
-  const size_t up_sizes[] = {4 * nw, nw, 4 * size_t(nd), size_t(nd), 32};
+  // one upload through pinned staging: xy | occ | control words (zeroed)
+  const size_t up_sizes[] = {8 * n, n, 4 * kCtlWords};
   size_t up = 0;
   for (size_t b : up_sizes) up += al(b);
   if (c->upd_host_n < up) {
@@ -458,37 +453,46 @@ static int apply_edits(rl_cddt* c, const int32_t* xy, const uint8_t* occ, size_t
     RL_CK(cudaMallocHost(&c->upd_host, up + up / 4));
     c->upd_host_n = up + up / 4;
   }
-  if (c->upd_up.n < up) RL_TRY(c->upd_up.alloc(up + up / 4));
-  size_t up_off[5];
-  {
-    uint8_t* hbuf = static_cast<uint8_t*>(c->upd_host);
-    const void* src[] = {wcells.data(), wflags.data(), dcells.data(), dsign.data(), nullptr};
-    size_t o = 0;
-    for (int k = 0; k < 5; k++) {
-      up_off[k] = o;
-      if (src[k] && up_sizes[k]) std::memcpy(hbuf + o, src[k], up_sizes[k]);
-      if (!src[k]) std::memset(hbuf + o, 0, up_sizes[k]);
-      o += al(up_sizes[k]);
-    }
-    RL_CK(cudaMemcpyAsync(c->upd_up.p, hbuf, up, cudaMemcpyHostToDevice, st));
-  }
-  const FlagEdits fe{reinterpret_cast<const int32_t*>(c->upd_up.p + up_off[0]),
-                     c->upd_up.p + up_off[1], int(nw)};
-  const EditBatch e{reinterpret_cast<const int32_t*>(c->upd_up.p + up_off[2]),
-                    reinterpret_cast<const int8_t*>(c->upd_up.p + up_off[3]), nd};
-  unsigned* ctl = reinterpret_cast<unsigned*>(c->upd_up.p + up_off[4]);
-  bool flags_done = false;
-  if (nd && c->gapped) {  // the touched rows only
+  // device scratch: the upload | changed cells (n) | delta cells (9n) | delta signs (9n)
+  const size_t dev_sizes[] = {up, 4 * n, 36 * n, 9 * n};
+  size_t need = 0;
+  for (size_t b : dev_sizes) need += al(b);
+  if (c->upd_up.n < need) RL_TRY(c->upd_up.alloc(need + need / 4));
+  uint8_t* hbuf = static_cast<uint8_t*>(c->upd_host);
+  std::memcpy(hbuf, xy, 8 * n);
+  std::memcpy(hbuf + al(8 * n), occ, n);
+  std::memset(hbuf + al(8 * n) + al(n), 0, 4 * kCtlWords);
+  RL_CK(cudaMemcpyAsync(c->upd_up.p, hbuf, up, cudaMemcpyHostToDevice, st));
+  const int32_t* d_xy = reinterpret_cast<const int32_t*>(c->upd_up.p);
+  const uint8_t* d_occ = c->upd_up.p + al(8 * n);
+  unsigned* ctl = reinterpret_cast<unsigned*>(c->upd_up.p + al(8 * n) + al(n));
+  int32_t* changed = reinterpret_cast<int32_t*>(c->upd_up.p + up);
+  int32_t* dcells = reinterpret_cast<int32_t*>(c->upd_up.p + up + al(4 * n));
+  int8_t* dsign = reinterpret_cast<int8_t*>(c->upd_up.p + up + al(4 * n) + al(36 * n));
+  const int nb = blocks_for(n, 256, 4);
+  k_replay_stamp<<<nb, 256, 0, st>>>(d_xy, int(n), c->w, c->estamp.p, gen);
+  k_replay_apply<<<nb, 256, 0, st>>>(d_xy, d_occ, int(n), c->w, c->estamp.p, gen, c->flags.p,
+                                     changed, ctl);
+  k_replay_flags<<<blocks_for(9 * n, 256, 4), 256, 0, st>>>(changed, c->w, c->h, c->wpr,
+                                                            c->wstamp.p, gen, c->flags.p,
+                                                            c->rowbits.p, dcells, dsign, ctl);
+  RL_CK(cudaGetLastError());
+  c->mirror_stale = true;
+  EditBatch e{dcells, dsign, ctl + kCtlDeltas, int(9 * n), -1};
+  if (c->gapped) {  // the touched rows only
     bool applied = false;
-    RL_TRY(edits_in_place(c, fe, e, ctl, &applied));
+    RL_TRY(edits_in_place(c, e, ctl, &applied));
     if (applied) return finish(c, nullptr);
-    flags_done = true;  // a row needs the relayout; the flags are in place
+  } else {
+    uint32_t* hs = nullptr;
+    RL_TRY(host_small(c, &hs));
+    RL_CK(cudaMemcpyAsync(hs, ctl, 4 * kCtlWords, cudaMemcpyDeviceToHost, st));
+    RL_CK(cudaStreamSynchronize(st));
   }
-  if (!flags_done) {
-    k_set_flags<<<blocks_for(nw, 256), 256, 0, st>>>(fe, c->w, c->wpr, c->flags.p, c->rowbits.p);
-    RL_CK(cudaGetLastError());
-  }
-  if (nd) RL_TRY(edits_relayout(c, e));
+  uint32_t* hs = nullptr;
+  RL_TRY(host_small(c, &hs));
+  e.n = int(hs[kCtlDeltas]);
+  if (e.n) RL_TRY(edits_relayout(c, e));
   return finish(c, nullptr);
 }
 
@@ -558,7 +562,10 @@ static int edits_relayout(rl_cddt* c, const EditBatch& e) {
   }();
   const size_t append = std::max(slots_ub / 4, size_t(1) << 20);
   const size_t slots_buf = std::min(slots_ub + append, (size_t(1) << 31) - 1);
-  if (c->zp_spare.n < slots_buf) RL_TRY(c->zp_spare.alloc(slots_buf));
+  // (with headroom: a structure that keeps growing would otherwise reallocate
+  // - a synchronous free and malloc of the whole array - at every relayout)
+  if (c->zp_spare.n < slots_buf)
+    RL_TRY(c->zp_spare.alloc(std::min(slots_buf + slots_buf / 4, (size_t(1) << 31) - 1)));
   k_merge_rows<<<blocks_for(rows * 32, 256, 32), 256, 0, st>>>(
       c->row_off.p, c->gapped ? c->row_len.p : nullptr, c->zp.p, packed_off, c->off_spare.p,
       c->zp_spare.p, add_cnt, rem_cnt, rec_v, rec_s, rows,
@@ -615,27 +622,18 @@ struct BucketView {
   uint32_t* pos;   // planned: a remove's claimed index, an add's insert position
   uint32_t* list;
   uint4* span;     // planned: {pmin, pend, net, new first slot or ~0u (in place)}
-  // ctl: list length, status (1: a bucket overflowed, 2: the append area is
-  // exhausted), missed removals, append slots reserved, net point change (i64)
-  unsigned* ctl;
+  unsigned* ctl;   // the batch's control words (kCtl*)
   long long* net;
 };
 
 // every (delta pixel, slice, row) record into its row's bucket; the first
-// record of a row lists the row. The leading blocks write the batch's flags.
-__global__ void k_flags_bucket(FlagEdits fe, int flag_blocks, int wpr, uint8_t* __restrict__ flags,
-                               uint2* __restrict__ bits, EditBatch e,
-                               const SliceParam* __restrict__ slices, int S, int w,
-                               BucketView b) {
-  if (int(blockIdx.x) < flag_blocks) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fe.n; i += flag_blocks * blockDim.x)
-      set_flag(fe, i, w, wpr, flags, bits);
-    return;
-  }
-  const int nb = gridDim.x - flag_blocks, bx = blockIdx.x - flag_blocks;
-  const int total = e.n * S;
-  for (int i = bx * blockDim.x + threadIdx.x; i < total; i += nb * blockDim.x) {
-    const int k = i / S, s = i % S;
+// record of a row lists the row
+__global__ void k_bucket(EditBatch e, const SliceParam* __restrict__ slices, int S, int w,
+                         BucketView b) {
+  const unsigned total = *e.n_dev * unsigned(S);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += gridDim.x * blockDim.x) {
+    const int k = int(i / S), s = int(i % S);
     const int cell = e.cells[k];
     const SliceParam sp = slices[s];
     int r0, r1;
@@ -644,12 +642,12 @@ __global__ void k_flags_bucket(FlagEdits fe, int flag_blocks, int wpr, uint8_t* 
     for (int r = r0; r <= r1; r++) {
       const uint32_t g = sp.row_base + uint32_t(r);
       const uint32_t slot = atomicAdd(&b.cnt[g], 1u);
-      if (slot == 0) b.list[atomicAdd(&b.ctl[0], 1u)] = g;
+      if (slot == 0) b.list[atomicAdd(&b.ctl[kCtlRows], 1u)] = g;
       if (slot < kBucket) {
         b.val[size_t(g) * kBucket + slot] = v;
         b.sgn[size_t(g) * kBucket + slot] = e.sign[k];
       } else {
-        atomicOr(&b.ctl[1], 1u);
+        atomicOr(&b.ctl[kCtlStatus], 1u);
       }
     }
   }
@@ -674,9 +672,8 @@ __device__ __forceinline__ bool middle_dest(const MergePlan& p, uint32_t i, floa
                                             uint32_t* dst) {
   bool removed = false;
   unsigned rb = 0, adds_lt = 0;
-  const unsigned any = p.add_mask | p.rem_mask;
-  for (unsigned l = 0; l < 32; l++) {
-    if (!((any >> l) & 1u)) continue;  // warp-uniform
+  for (unsigned any = p.add_mask | p.rem_mask; any; any &= any - 1) {  // warp-uniform
+    const unsigned l = __ffs(any) - 1;
     const uint32_t pl = __shfl_sync(0xffffffffu, p.pos, l);
     const float dl = __shfl_sync(0xffffffffu, p.dv, l);
     if ((p.rem_mask >> l) & 1u) {
@@ -695,9 +692,8 @@ __device__ __forceinline__ bool middle_dest(const MergePlan& p, uint32_t i, floa
 __device__ __forceinline__ uint32_t add_dest(const MergePlan& p) {
   const unsigned lane = threadIdx.x & 31;
   unsigned rem_lt = 0, adds_before = 0;
-  const unsigned any = p.add_mask | p.rem_mask;
-  for (unsigned l = 0; l < 32; l++) {
-    if (!((any >> l) & 1u)) continue;
+  for (unsigned any = p.add_mask | p.rem_mask; any; any &= any - 1) {  // warp-uniform
+    const unsigned l = __ffs(any) - 1;
     const uint32_t pl = __shfl_sync(0xffffffffu, p.pos, l);
     const float dl = __shfl_sync(0xffffffffu, p.dv, l);
     if ((p.rem_mask >> l) & 1u)
@@ -717,8 +713,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) k_bucket_plan(
     const uint32_t* __restrict__ len, const float* __restrict__ zp, uint32_t append_base,
     uint32_t slots_total) {
   const unsigned lane = threadIdx.x & 31, lt = (1u << lane) - 1;
-  const unsigned m = b.ctl[0];
-  if (b.ctl[1]) return;  // a bucket overflowed: relayout
+  const unsigned m = b.ctl[kCtlRows];
+  if (b.ctl[kCtlStatus]) return;  // a bucket overflowed: relayout
   const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
   for (unsigned j = warp; j < m; j += nwarps) {
@@ -759,9 +755,9 @@ __global__ void __launch_bounds__(32 * kMergeWarps) k_bucket_plan(
       uint32_t target = ~0u;
       if (nn > cap[g] || pend - pmin > uint32_t(kMidMax)) {
         const uint32_t need = slot_capacity(nn);
-        const uint32_t at = atomicAdd(&b.ctl[3], need);
+        const uint32_t at = atomicAdd(&b.ctl[kCtlAppend], need);
         if (uint64_t(append_base) + at + need > slots_total)
-          atomicOr(&b.ctl[1], 2u);
+          atomicOr(&b.ctl[kCtlStatus], 2u);
         else
           target = append_base + at;
       }
@@ -778,8 +774,8 @@ __global__ void __launch_bounds__(32 * kMergeWarps) k_merge_touched(
     BucketView b, uint32_t* __restrict__ off, uint32_t* __restrict__ cap,
     uint32_t* __restrict__ len, float* __restrict__ zp, float* __restrict__ hints) {
   const unsigned lane = threadIdx.x & 31;
-  const unsigned m = b.ctl[0];
-  const bool skip = b.ctl[1] != 0;
+  const unsigned m = b.ctl[kCtlRows];
+  const bool skip = b.ctl[kCtlStatus] != 0;
   const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
   long long net = 0;
@@ -882,11 +878,10 @@ __global__ void __launch_bounds__(32 * kMergeWarps) k_merge_touched(
   }
   if (lane == 0 && net)
     atomicAdd(reinterpret_cast<unsigned long long*>(b.net), static_cast<unsigned long long>(net));
-  if (missed) atomicAdd(&b.ctl[2], missed);
+  if (missed) atomicAdd(&b.ctl[kCtlMissed], missed);
 }
 
-static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, unsigned* ctl,
-                          bool* applied) {
+static int edits_in_place(rl_cddt* c, const EditBatch& e, unsigned* ctl, bool* applied) {
   *applied = false;
   cudaStream_t st = c->stream;
   const size_t rows = c->rows;
@@ -913,11 +908,9 @@ static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, u
   b.list = reinterpret_cast<uint32_t*>(take(sizes[4]));
   b.span = reinterpret_cast<uint4*>(take(sizes[5]));
   b.ctl = ctl;
-  b.net = reinterpret_cast<long long*>(ctl + 4);
-  const int fb = blocks_for(size_t(fe.n), 256, 2);
-  const int bb = blocks_for(size_t(e.n) * c->S, 256);
-  k_flags_bucket<<<fb + bb, 256, 0, st>>>(fe, fb, c->wpr, c->flags.p, c->rowbits.p, e,
-                                          c->d_slices.p, c->S, c->w, b);
+  b.net = reinterpret_cast<long long*>(ctl + kCtlNet);
+  k_bucket<<<blocks_for(size_t(e.n_bound) * c->S, 256), 256, 0, st>>>(e, c->d_slices.p, c->S,
+                                                                       c->w, b);
   // latency-bound warps (a chain of dependent loads per row): fill the GPU
   static const int plan_ctas = [] {
     int per_sm = 0;
@@ -937,22 +930,22 @@ static int edits_in_place(rl_cddt* c, const FlagEdits& fe, const EditBatch& e, u
   RL_CK(cudaGetLastError());
   uint32_t* hs = nullptr;
   RL_TRY(host_small(c, &hs));
-  RL_CK(cudaMemcpyAsync(hs, ctl, 32, cudaMemcpyDeviceToHost, st));
+  RL_CK(cudaMemcpyAsync(hs, ctl, 4 * kCtlWords, cudaMemcpyDeviceToHost, st));
   RL_CK(cudaStreamSynchronize(st));
 #ifdef RL_EDIT_PROFILE
-  fprintf(stderr, "in-place status %u rows %u appended %u of %zu free\n", hs[1], hs[0], hs[3],
+  fprintf(stderr, "in-place status %u rows %u appended %u of %zu free\n", hs[kCtlStatus], hs[kCtlRows], hs[kCtlAppend],
           size_t(c->zp.n - c->zp_slots));
 #endif
-  if (hs[1]) return RL_OK;  // nothing written: relayout
-  if (hs[2]) {
+  if (hs[kCtlStatus]) return RL_OK;  // nothing written: relayout
+  if (hs[kCtlMissed]) {
     set_error("cddt: %u zero-point removals found no stored point (structure inconsistent)",
-              hs[2]);
+              hs[kCtlMissed]);
     return RL_ELOGIC;
   }
   long long net = 0;
-  std::memcpy(&net, hs + 4, 8);
+  std::memcpy(&net, hs + kCtlNet, 8);
   c->zero_points = uint64_t((long long)c->zero_points + net);
-  c->zp_slots += hs[3];
+  c->zp_slots += hs[kCtlAppend];
   *applied = true;
   return RL_OK;
 }
