@@ -799,3 +799,27 @@ def test_edit_paths_in_place_relocated_relayout(append):
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().split()[0] == "EQUAL", r.stdout + r.stderr[-2000:]
+
+
+def test_edit_batch_larger_than_a_chunk(rl, oracle_mod):
+    """A batch of more than 2^20 edits is replayed in order in chunks (the
+    device stamp keeps 20 bits of edit index): the last edit of each cell
+    wins across the chunk boundary, and the structure equals a fresh build of
+    the final grid (proj/tests/test_cddt.cpp:578-604)."""
+    g = random_map(64, 48, 0.2, 21)
+    K = 16
+    gpu = make_gpu(rl, g, K)
+    rng = np.random.default_rng(77)
+    n = (1 << 20) + 4099
+    xy = np.stack([rng.integers(0, 64, n), rng.integers(0, 48, n)], 1).astype(np.int32)
+    occ = rng.integers(0, 2, n).astype(np.uint8)
+    # cells whose last edit lies past the chunk boundary and whose earlier ones differ
+    xy[-3:] = [[5, 5], [6, 6], [5, 5]]
+    xy[:2] = [[5, 5], [6, 6]]
+    occ[:2], occ[-3:] = [1, 1], [1, 0, 0]
+    final = np.array(g, np.uint8, copy=True)
+    final[xy[:, 1], xy[:, 0]] = occ  # numpy keeps the last write per index
+    assert final[5, 5] == 0 and final[6, 6] == 0
+    gpu.set_occupancy_batch(xy, occ)
+    assert np.array_equal(gpu.export()["grid"], final)
+    assert_same_structure(gpu, oracle_mod.OracleCddt(final, K).export())
