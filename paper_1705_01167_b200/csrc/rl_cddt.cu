@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(256) k_prune_mark(CddtView c, uint8_t* __restr
     if (__ldg(c.flags + cell) & kOcc) continue;  // occupied origins never consult bins
     const int cx = int(cell % c.w), cy = int(cell / c.w);
     CastOut o;
-    directional_cast(c, double(cx) + 0.5, double(cy) + 0.5, a, o);
+    directional_cast(c, double(cx) + 0.5, double(cy) + 0.5, a, o, false);  // resolving index only
     if (o.res_idx < 0) continue;
     const uint32_t lo = c.row_off[o.res_g], n = c.row_off[o.res_g + 1] - lo;
     uint8_t* m = marks + lo;

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict
     const double x = double(__ldcs(qx + i)), y = double(__ldcs(qy + i));
     const double th = normalize_angle_2pi(double(__ldcs(qt + i)));  // RayQuery ctor, raycast.hpp:47
     CastOut o;
-    const double r = directional_cast(c, x, y, direction_index(th, c.K), o);
+    const double r = directional_cast(c, x, y, direction_index(th, c.K), o, HIT);
     if (out) __stcs(out + i, T(r));
     if (HIT && hit) hit[i] = o.hit;
     if (RES) {
@@ -515,7 +515,7 @@ __global__ void k_directional(CddtView c, const double* __restrict__ x,
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x) {
     CastOut o;
-    out[i] = directional_cast(c, x[i], y[i], a[i], o);
+    out[i] = directional_cast(c, x[i], y[i], a[i], o, false);
   }
 }
 
@@ -524,7 +524,7 @@ __global__ void k_single(CddtView c, double x, double y, double theta, int pair,
   const double th = normalize_angle_2pi(theta);
   const int a = direction_index(th, c.K);
   CastOut o;
-  out[0] = directional_cast(c, x, y, a, o);
+  out[0] = directional_cast(c, x, y, a, o, false);
   if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
 }
 

@@ -361,6 +361,9 @@ __device__ __forceinline__ double pair_side(const CddtView& c, double x, double 
     if (d >= c.max_range) break;
     int32_t cell;
     if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) return d;
+#if RL_PROBE_SENSOR
+    if (window_probe_hit(c, x, y, dir.x, dir.y, d)) return d;
+#endif
     if (!have_walker) {
       wk.init_at(x, y, dir, d - kVerifyHalf);
       have_walker = true;
