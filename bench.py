@@ -577,6 +577,7 @@ def cpu_model():
 
 # ---------------------------------------------------------------- arms
 def run_ours(args, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -634,6 +635,23 @@ def run_ours(args, rank, world, local_rank):
 
     value = world * n * args.steps / t_dev
     e2e_value = world * n * args.e2e_steps / t_e2e
+    e2e_pageable = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        # the same call with PAGEABLE buffers (what a reference caller holds): staged through
+        # a pinned ring by host threads inside the library; the call is synchronous, wall clock
+        px, py, pt = (np.array(a, copy=True) for a in (hx, hy, ht))
+        po = np.zeros(n, dtype=np.float32)
+        cddt.cast_batch(px, py, pt, out=po)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            cddt.cast_batch(px, py, pt, out=po)
+        t_pg = time.perf_counter() - t0
+        if not np.array_equal(po, ho):
+            raise RuntimeError("pageable and pinned host-path results differ")
+        e2e_pageable = {"value": n * args.e2e_steps / t_pg, "unit": UNIT,
+                        "path": "rl_cddt_cast_batch_host (pageable numpy buffers, staged through "
+                                "a pinned ring by host threads with non-temporal copies)"}
+        del px, py, pt, po
     line = None
     sharded_pf = None
     if world > 1 and args.pf_iterations > 0:  # every rank: the sharded filter
@@ -688,7 +706,8 @@ def run_ours(args, rank, world, local_rank):
                            build_plus_prune_s=round(info.init_seconds, 3)),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 12 * n,
                     "d2h_bytes_per_step": 4 * n, "steps": args.e2e_steps,
-                    "path": "rl_cddt_cast_batch_host (pinned host buffers, 3-stream pipeline)"},
+                    "path": "rl_cddt_cast_batch_host (pinned host buffers, 3-stream pipeline)",
+                    "pageable": e2e_pageable},
             # per step: two pipelines (one per half of the batch) of k_cast_defer_p1,
             # k_cast_near and four k_walk_pass window passes
             "gpu_launches": 12 * args.steps,

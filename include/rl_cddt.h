@@ -101,9 +101,14 @@ int rl_cddt_cast_batch_f64(rl_cddt *c, const double *x, const double *y, const d
 int rl_cddt_directional_batch(rl_cddt *c, const double *x, const double *y, const int32_t *a,
                               double *out, size_t n, void *stream);
 
-/* Host-memory batched casts: host -> device copies, kernel and device -> host
- * copies pipelined in chunks over several streams. Pinned host buffers give
- * full PCIe bandwidth; pageable ones work but copy slower. */
+/* Host-memory batched casts (the per-query loop of run_batches, proj/src/bench.cpp:86-106,
+ * over caller-owned arrays): host -> device copies, kernel and device -> host
+ * copies pipelined in chunks over several streams. Page-locked (pinned or
+ * registered) buffers are copied directly at full PCIe bandwidth. Pageable
+ * buffers (plain vectors) of >= 2^20 queries are staged through a ring of pinned
+ * buffers by a few host threads (RL_HOST_COPY_THREADS, default min(8, cores/2))
+ * instead of the driver's synchronous bounce copy: about two thirds of the
+ * pinned rate. Blocking: results are in `out` on return. */
 int rl_cddt_cast_batch_host(rl_cddt *c, const float *x, const float *y, const float *theta,
                             float *out, size_t n);
 

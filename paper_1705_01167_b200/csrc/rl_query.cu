@@ -3,6 +3,11 @@
 // everything else, and the query entry points of the C ABI (include/rl_cddt.h).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <thread>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 #include <vector>
 
 #include "rl_common.cuh"
@@ -537,6 +542,175 @@ static int dir_blocks(size_t n) {
 
 using namespace rl;
 
+// ---------------------------------------------------------------------------
+// Pageable host buffers (what a reference caller holds: std::vector<RayQuery>
+// fields, numpy arrays). cudaMemcpyAsync from pageable memory is staged by the
+// driver through one bounce buffer, synchronously: 134 ms per 100M queries
+// against 24 ms from pinned memory. Here the chunks are staged through a ring
+// of pinned buffers by a few host threads (plain memcpy) while the DMA engines
+// and the kernels work on the other lanes' chunks.
+constexpr size_t kStageMinQueries = size_t(1) << 20;  // below: one driver-staged copy is as fast
+
+// true when the DMA engines can read/write the range directly (page-locked,
+// registered, managed or device memory)
+static bool dma_direct(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type != cudaMemoryTypeUnregistered;
+}
+
+struct CopySeg {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
+// memcpy with non-temporal stores: the destination is not read for ownership
+// and does not displace the source from the caches (a staging copy is written
+// once and read by the DMA engine, or by the caller much later)
+static void stream_copy(char* dst, const char* src, size_t bytes) {
+#if defined(__x86_64__) && defined(__SSE2__)
+  static const bool nt = [] {
+    const char* e = std::getenv("RL_HOST_NT");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (nt && bytes >= 4096) {
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    bytes -= head;
+    size_t k = 0;
+    for (; k + 64 <= bytes; k += 64) {
+      const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k));
+      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 16));
+      const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 32));
+      const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 48));
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k), a);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 16), b);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 32), c);
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 48), d);
+    }
+    _mm_sfence();
+    std::memcpy(dst + k, src + k, bytes - k);
+    return;
+  }
+#endif
+  std::memcpy(dst, src, bytes);
+}
+
+// the segments copied by `threads` host threads, each taking an equal slice of
+// every segment (the caller's thread is one of them)
+static void parallel_copy(const std::vector<CopySeg>& segs, int threads) {
+  auto work = [&segs, threads](int t) {
+    for (const CopySeg& g : segs) {
+      const size_t per = ((g.bytes + size_t(threads) - 1) / size_t(threads) + 63) & ~size_t(63);
+      const size_t a = std::min(g.bytes, per * size_t(t)), b = std::min(g.bytes, a + per);
+      if (b > a) stream_copy(static_cast<char*>(g.dst) + a, static_cast<const char*>(g.src) + a, b - a);
+    }
+  };
+  std::vector<std::thread> pool;
+  pool.reserve(size_t(threads > 1 ? threads - 1 : 0));
+  for (int t = 1; t < threads; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+}
+
+static int cast_batch_staged(rl_cddt* c, const float* x, const float* y, const float* theta,
+                             float* out, size_t n) {
+  constexpr int NSTREAM = 3;
+  static const int threads = [] {
+    const char* e = std::getenv("RL_HOST_COPY_THREADS");
+    const int hw = int(std::thread::hardware_concurrency());
+    return std::max(1, e ? std::atoi(e) : std::min(8, hw > 1 ? hw / 2 : 1));
+  }();
+  static const size_t chunk_max = [] {
+    const char* e = std::getenv("RL_HOST_STAGE_CHUNK_LOG2");
+    return size_t(1) << (e ? std::atoi(e) : 22);  // 4M queries: the split pipeline's minimum
+  }();
+  const size_t chunk = std::min(n, chunk_max);
+  struct Lane {
+    cudaStream_t s = nullptr;
+    DevBuf<float> dev;      // x | y | theta | out
+    float* pin = nullptr;   // the same layout in page-locked host memory
+    size_t pend_off = 0, pend_m = 0;  // results waiting in pin's out block
+    ~Lane() {
+      if (pin) cudaFreeHost(pin);
+      if (s) cudaStreamDestroy(s);
+    }
+  };
+  static thread_local std::vector<Lane> lanes;  // reused across calls on this thread
+  static thread_local size_t lane_chunk = 0;
+  static thread_local int lane_dev = -1;
+  if (lanes.empty() || lane_chunk < chunk || lane_dev != c->dev) {
+    lanes.clear();
+    lanes = std::vector<Lane>(NSTREAM);
+    lane_chunk = 0;
+    for (auto& l : lanes) {
+      RL_CK(cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking));
+      RL_TRY(l.dev.alloc(4 * chunk));
+      RL_CK(cudaHostAlloc(reinterpret_cast<void**>(&l.pin), 4 * chunk * sizeof(float),
+                          cudaHostAllocDefault));
+    }
+    lane_chunk = chunk;
+    lane_dev = c->dev;
+  }
+  for (auto& l : lanes) l.pend_m = 0;
+  cudaEvent_t ready;
+  RL_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  struct EventGuard {  // released on every return path
+    cudaEvent_t e;
+    ~EventGuard() { cudaEventDestroy(e); }
+  } ready_guard{ready};
+  RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
+  const size_t stride = lane_chunk;
+  std::vector<CopySeg> segs;
+  size_t k = 0;
+  for (size_t off = 0; off < n; k++) {
+    // the first chunks are small so the link starts early; the rest are full
+    const size_t m = std::min(n - off, k < 2 ? std::max<size_t>(chunk >> (2 - k), 1) : chunk);
+    Lane& l = lanes[k % NSTREAM];
+    segs.clear();
+    if (l.pend_m) {  // the lane's previous results leave its pinned block first
+      RL_CK(cudaStreamSynchronize(l.s));
+      segs.push_back({out + l.pend_off, l.pin + 3 * stride, l.pend_m * sizeof(float)});
+    }
+    segs.push_back({l.pin, x + off, m * sizeof(float)});
+    segs.push_back({l.pin + stride, y + off, m * sizeof(float)});
+    segs.push_back({l.pin + 2 * stride, theta + off, m * sizeof(float)});
+    parallel_copy(segs, threads);
+    float* dx = l.dev.p;
+    RL_CK(cudaStreamWaitEvent(l.s, ready, 0));
+    if (m == stride) {  // x | y | theta are contiguous: one copy
+      RL_CK(cudaMemcpyAsync(dx, l.pin, 3 * m * sizeof(float), cudaMemcpyHostToDevice, l.s));
+    } else {
+      for (int a = 0; a < 3; a++)
+        RL_CK(cudaMemcpyAsync(dx + a * stride, l.pin + a * stride, m * sizeof(float),
+                              cudaMemcpyHostToDevice, l.s));
+    }
+    RL_TRY(launch_cast<float>(c, dx, dx + stride, dx + 2 * stride, dx + 3 * stride, nullptr,
+                              nullptr, nullptr, m, l.s, true));
+    RL_CK(cudaGetLastError());
+    RL_CK(cudaMemcpyAsync(l.pin + 3 * stride, dx + 3 * stride, m * sizeof(float),
+                          cudaMemcpyDeviceToHost, l.s));
+    l.pend_off = off;
+    l.pend_m = m;
+    off += m;
+  }
+  // drain in submission order
+  for (size_t j = (k >= NSTREAM ? k - NSTREAM : 0); j < k; j++) {
+    Lane& l = lanes[j % NSTREAM];
+    if (!l.pend_m) continue;
+    RL_CK(cudaStreamSynchronize(l.s));
+    parallel_copy({{out + l.pend_off, l.pin + 3 * stride, l.pend_m * sizeof(float)}}, threads);
+    l.pend_m = 0;
+  }
+  return RL_OK;
+}
+
 extern "C" {
 
 // One query (Cddt::cast / cast_pair): a one-thread kernel that writes its
@@ -599,12 +773,20 @@ int rl_cddt_directional_batch(rl_cddt* c, const double* x, const double* y, cons
 }
 
 // Host-buffer batches: chunked H2D -> kernel -> D2H over NSTREAM streams so
-// both copy directions overlap the kernel.
+// both copy directions overlap the kernel. Page-locked buffers are copied from
+// and to directly; pageable ones go through cast_batch_staged above.
 int rl_cddt_cast_batch_host(rl_cddt* c, const float* x, const float* y, const float* theta,
                             float* out, size_t n) {
   if (!c || (n && (!x || !y || !theta || !out))) return RL_EINVAL;
   if (n == 0) return RL_OK;
   DeviceGuard guard(c->dev);
+  static const bool stage_pageable = [] {
+    const char* e = std::getenv("RL_HOST_STAGE");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  if (stage_pageable && n >= kStageMinQueries &&
+      !(dma_direct(x) && dma_direct(y) && dma_direct(theta) && dma_direct(out)))
+    return cast_batch_staged(c, x, y, theta, out, n);
   constexpr int NSTREAM = 3;
   const size_t chunk = std::min<size_t>(n, size_t(1) << 23);  // 8M queries = 128 MB per chunk
   struct Lane {

@@ -823,3 +823,27 @@ def test_edit_batch_larger_than_a_chunk(rl, oracle_mod):
     gpu.set_occupancy_batch(xy, occ)
     assert np.array_equal(gpu.export()["grid"], final)
     assert_same_structure(gpu, oracle_mod.OracleCddt(final, K).export())
+
+
+def test_host_path_pageable_pinned_and_mixed(rl, synth):
+    """rl_cddt_cast_batch_host with pageable buffers (staged through the pinned
+    ring by host threads), pinned buffers (copied directly) and a mix, at sizes
+    around the staging chunk (ragged last chunk, fewer chunks than lanes): all
+    equal the device-pointer path bit for bit."""
+    import torch
+    g = synth.rect_map(300, 260, 14, seed=4)
+    gpu = make_gpu(rl, g, 108, 200.0)
+    nmax = (9 << 20) + 12345
+    qx, qy, qt = synth.free_queries(g, nmax, seed=21)
+    want = host(gpu.cast_batch(dev(qx), dev(qy), dev(qt)))
+    torch.cuda.synchronize()
+    pin = [torch.from_numpy(a).pin_memory().numpy() for a in (qx, qy, qt)]
+    for n in (nmax, (4 << 20), (1 << 20) + 7, 1000):
+        got = gpu.cast_batch(qx[:n], qy[:n], qt[:n])  # pageable in, pageable out
+        assert np.array_equal(got.view(np.uint32), want[:n].view(np.uint32)), n
+        out = torch.empty(n, dtype=torch.float32).pin_memory().numpy()
+        gpu.cast_batch(pin[0][:n], pin[1][:n], pin[2][:n], out=out)  # all pinned
+        assert np.array_equal(out.view(np.uint32), want[:n].view(np.uint32)), n
+        out2 = np.zeros(n, dtype=np.float32)
+        gpu.cast_batch(pin[0][:n], qy[:n], pin[2][:n], out=out2)  # mixed
+        assert np.array_equal(out2.view(np.uint32), want[:n].view(np.uint32)), n
