@@ -639,8 +639,14 @@ struct WalkDefer {
   float cval;      // its zero point (phase 1 loaded it)
 };
 
-__device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x, double y, int a,
+// Register diet (32 registers, no spills, so 2048 resident threads per SM
+// instead of 1536; -1 % per step): the query enters as floats and its doubles
+// are rebuilt (exactly) after the row search; the direction and the projected
+// x' are not kept across the search either - the 32-byte per-direction entry
+// is read again (an L1 hit) and x' recomputed with the same operations.
+__device__ __forceinline__ bool directional_cast_p1(const CddtView& c, float xf, float yf, int a,
                                                     double* result, WalkDefer* def) {
+  double x = double(xf), y = double(yf);
   const int cxi = (int)floor(x), cyi = (int)floor(y);
   if (!in_bounds(c, cxi, cyi)) {
     *result = c.max_range;
@@ -664,12 +670,22 @@ __device__ __forceinline__ bool directional_cast_p1(const CddtView& c, double x,
   const RowSearch rs =
       partition_point_hinted(c.zp + q.lo, q.hi - q.lo, q.xq, q.forward, q.hint, q.hint2);
   const int n = (int)(q.hi - q.lo);
-  const int step = q.forward ? 1 : -1;
-  for (int idx = q.forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
+  const bool forward = a < c.S;
+  const int step = forward ? 1 : -1;
+  for (int idx = forward ? (int)rs.first : (int)rs.first - 1; idx >= 0 && idx < n;
        idx += step) {
     const float fv = uint32_t(idx) == rs.kidx ? rs.kval : __ldg(c.zp + q.lo + idx);
     const double vv = (double)fv;
-    const double d = q.forward ? vv - q.xq : q.xq - vv;
+    // the barrier keeps the compiler from holding the first conversion's doubles
+    asm volatile("" : "+f"(xf), "+f"(yf));
+    x = double(xf);
+    y = double(yf);
+    double pcs, psn;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(pcs), "=d"(psn), "=d"(dir.x), "=d"(dir.y)
+                 : "l"(c.pdirs + a));
+    const double xq = x * pcs + y * psn;  // cddt.hpp:31, as in query_row
+    const double d = forward ? vv - xq : xq - vv;
     if (d >= c.max_range) break;
     int32_t cell;
     if (landing_hit(c, x + d * dir.x, y + d * dir.y, &cell)) {

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <type_traits>
 #if defined(__x86_64__)
 #include <emmintrin.h>
 #endif
@@ -74,7 +75,7 @@ __device__ __forceinline__ void st256_cs(void* p, const float4& a, const float4&
 }
 
 #ifndef RL_P1_CTAS
-#define RL_P1_CTAS 6  // resident CTAs per SM the register budget of phase 1 targets
+#define RL_P1_CTAS 8  // resident 256-thread equivalents per SM the register budget of phase 1 targets (32 registers)
 #endif
 #ifndef RL_P2_CTAS
 #define RL_P2_CTAS 4
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
       }
     }
     bool defer = false;
-    WalkRecord rec;
+    WalkRecord rec{};  // defined on every path: no stale fields to keep (or spill) across iterations
     if (i < n) {
       rec.x = __ldcs(qx + i);
       rec.y = __ldcs(qy + i);
@@ -119,8 +120,7 @@ __global__ void __launch_bounds__(kP1Threads, RL_P1_CTAS * 256 / kP1Threads) k_c
       const double th = normalize_angle_2pi(double(rec.t));
       double r;
       WalkDefer def;
-      if (directional_cast_p1(c, double(rec.x), double(rec.y), direction_index(th, c.K), &r,
-                              &def)) {
+      if (directional_cast_p1(c, rec.x, rec.y, direction_index(th, c.K), &r, &def)) {
         __stcs(out + i, T(r));
       } else {
         defer = true;
@@ -375,7 +375,10 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     const char* e = std::getenv("RL_SPLIT_PARTS");
     return e ? std::max(1, std::atoi(e)) : 2;
   }();
-  if (split && parts > 1 && !rr && !ri && !hit && small && n >= kDeferMinQueries * parts) {
+  // the split pipeline's records hold the query as floats: f32 batches only
+  // (f64 queries need not be float-representable; they take k_cast)
+  constexpr bool kF32 = std::is_same<T, float>::value;
+  if (kF32 && split && parts > 1 && !rr && !ri && !hit && small && n >= kDeferMinQueries * parts) {
     // two independent pipelines over the halves of the batch, on the caller's
     // stream and a forked one: the late, thinly occupied window passes of one
     // overlap the other's phase 1
@@ -403,7 +406,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     RL_CK(cudaStreamWaitEvent(st, pp.join, 0));
     return RL_OK;
   }
-  if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
+  if constexpr (kF32) if (!rr && !ri && !hit && small && n >= kDeferMinQueries) {
     // stream-ordered scratch: concurrent batches on other streams (e.g. the
     // pipelined host path) each get their own queue; the pool keeps the
     // memory reserved, so steady-state allocation is free

@@ -83,3 +83,34 @@ def test_degenerate_and_ragged_maps(rl, oracle_mod, shape):
         p = rl.Cddt(rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(0.0, 36), prune=prune)
         o.prune()
         assert np.array_equal(p.export()["zp"].view(np.uint32), o.export()["zp"].view(np.uint32))
+
+
+def test_f64_batch_above_split_threshold_keeps_double_queries(rl, oracle_mod, synth):
+    """A >= 4M f64 batch with range output only must not go through the split
+    pipeline (its records hold the query as floats): genuinely double
+    coordinates give the same bits as the single-kernel path with hit cells,
+    and as the reference / restatement on a sample."""
+    import torch
+    g = synth.rect_map(300, 260, 14, seed=4)
+    c = rl.Cddt(rl.OccupancyGrid.from_array(g), rl.RangeMethodConfig(200.0, 108))
+    n = (1 << 22) + 4097
+    qx, qy, qt = synth.free_queries(g, n, seed=33)
+    rng = np.random.default_rng(5)
+    x = qx.astype(np.float64) + rng.uniform(-1e-4, 1e-4, n)  # not float-representable
+    y = qy.astype(np.float64) + rng.uniform(-1e-4, 1e-4, n)
+    t = qt.astype(np.float64) + rng.uniform(-1e-6, 1e-6, n)
+    dx, dy, dt = (torch.from_numpy(a).cuda() for a in (x, y, t))
+    a = c.cast_batch_f64(dx, dy, dt)
+    hit = torch.empty(n, dtype=torch.int32, device="cuda")
+    b = c.cast_batch_f64(dx, dy, dt, hit=hit)
+    torch.cuda.synchronize()
+    a, b = a.cpu().numpy(), b.cpu().numpy()
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    m = 20_000
+    if oracle_mod.ref_available():
+        want, _ = oracle_mod.RefCddt(g, 108, 200.0).cast_pair_batch(x[:m], y[:m], t[:m])
+    else:
+        o = oracle_mod.OracleCddt(g, 108, 200.0)
+        m = 2_000
+        want = np.array([o.cast(x[i], y[i], t[i]) for i in range(m)])
+    assert np.array_equal(a[:m].view(np.uint64), np.asarray(want).view(np.uint64))
