@@ -77,9 +77,6 @@ __device__ __forceinline__ void st256_cs(void* p, const float4& a, const float4&
 #ifndef RL_P1_CTAS
 #define RL_P1_CTAS 8  // resident 256-thread equivalents per SM the register budget of phase 1 targets (32 registers)
 #endif
-#ifndef RL_P2_CTAS
-#define RL_P2_CTAS 4
-#endif
 #ifndef RL_WIN_CAPS
 #define RL_WIN_CAPS 1, 2, 4  // windows per query in each capped window pass; a last pass finishes
 #endif
@@ -177,6 +174,14 @@ struct __align__(16) ContRecord {
 #define RL_WALK_THREADS 64  // small CTAs: cheap compaction barriers
 #endif
 constexpr int kWalkThreads = RL_WALK_THREADS;
+// resident CTAs per SM the walk kernels' register budget targets: 18 x 64
+// threads at 56 registers without spills (16 at 60-62 registers: +0.4 % per
+// step; 20 at 48 registers spills: +3 %)
+#ifdef RL_P2_MINCTAS
+constexpr int kWalkMinCtas = RL_P2_MINCTAS;
+#else
+constexpr int kWalkMinCtas = 18;
+#endif
 
 // out-of-line: the rare overflow path must not add to the pass's registers
 __device__ __noinline__ double finish_windows(const CddtView& c, double x, double y, int a,
@@ -187,7 +192,7 @@ __device__ __noinline__ double finish_windows(const CddtView& c, double x, doubl
 }
 
 template <class T, bool CONT, bool LAST>
-__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_walk_pass(
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinCtas) k_walk_pass(
     CddtView c, const void* __restrict__ in, const unsigned* __restrict__ in_count,
     uint32_t in_cap, int cap, ContRecord* __restrict__ oq, unsigned* __restrict__ out_count,
     uint32_t out_cap, T* __restrict__ out) {
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads)
 // probes here; queries that need a verification window join the window
 // passes as continuations (queue A, after pass 0's own).
 template <class T>
-__global__ void __launch_bounds__(kWalkThreads, RL_P2_CTAS * 256 / kWalkThreads) k_cast_near(
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinCtas) k_cast_near(
     CddtView c, const WalkRecord* __restrict__ q, const unsigned* __restrict__ qn, uint32_t n,
     ContRecord* __restrict__ oq, unsigned* __restrict__ out_count, uint32_t out_cap,
     T* __restrict__ out) {
