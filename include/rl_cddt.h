@@ -112,6 +112,13 @@ int rl_cddt_directional_batch(rl_cddt *c, const double *x, const double *y, cons
 int rl_cddt_cast_batch_host(rl_cddt *c, const float *x, const float *y, const float *theta,
                             float *out, size_t n);
 
+/* The per-query loop of run_batches (proj/src/bench.cpp:86-106) over an array of
+ * n RayQuery {double x, y, theta} (proj/include/rangelib/raycast.hpp:42-49) in
+ * host memory, e.g. std::vector<RayQuery>::data(): out[i] = cast(queries[i]),
+ * bit for bit. Chunks are pipelined over three streams; a pageable array is
+ * staged through pinned buffers by host threads. Blocking. */
+int rl_cddt_cast_queries_host(rl_cddt *c, const double *queries, double *out, size_t n);
+
 /* Cddt::set_occupancy (cddt.cpp:332-377). */
 int rl_cddt_set_occupancy(rl_cddt *c, int32_t x, int32_t y, int32_t occupied);
 

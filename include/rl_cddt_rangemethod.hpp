@@ -84,6 +84,11 @@ class GpuCddtMethod final : public rangelib::RangeMethod {
   void cast_batch(const float* x, const float* y, const float* theta, float* out, size_t n) const {
     throw_on(rl_cddt_cast_batch_host(h_, x, y, theta, out, n));
   }
+  // run_batches' inner loop (proj/src/bench.cpp:86-106) as one call: out[i] = cast(q[i])
+  void cast_many(const rangelib::RayQuery* q, size_t n, double* out) const {
+    static_assert(sizeof(rangelib::RayQuery) == 3 * sizeof(double), "RayQuery is {x, y, theta}");
+    throw_on(rl_cddt_cast_queries_host(h_, reinterpret_cast<const double*>(q), out, n));
+  }
   // Cddt::set_occupancy (proj/src/cddt.cpp:332-377)
   void set_occupancy(int x, int y, bool occupied) {
     throw_on(rl_cddt_set_occupancy(h_, x, y, occupied ? 1 : 0));

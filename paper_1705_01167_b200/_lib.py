@@ -65,6 +65,7 @@ _SIG = {
     "rl_cddt_cast_batch_f64": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "rl_cddt_directional_batch": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, _P]),
     "rl_cddt_cast_batch_host": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t]),
+    "rl_cddt_cast_queries_host": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "rl_cddt_set_occupancy": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32]),
     "rl_cddt_set_occupancy_batch": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "rl_cddt_export": (C.c_int, [_P, _P, _P, _P, _P, _P]),

@@ -541,6 +541,19 @@ __global__ void k_single(CddtView c, double x, double y, double theta, int pair,
   if (pair) out[1] = directional_cast(c, x, y, (a + c.K / 2) % c.K, o);  // cddt.cpp:275-279
 }
 
+// The per-query loop of run_batches (proj/src/bench.cpp:86-106) over an array
+// of RayQuery {double x, y, theta} (raycast.hpp:42-49), read in place.
+__global__ void __launch_bounds__(256, 4) k_cast_queries(CddtView c, const double* __restrict__ q,
+                                                         double* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double x = __ldcs(q + 3 * i), y = __ldcs(q + 3 * i + 1);
+    const double th = normalize_angle_2pi(__ldcs(q + 3 * i + 2));  // RayQuery ctor (idempotent)
+    CastOut o;
+    __stcs(out + i, directional_cast(c, x, y, direction_index(th, c.K), o, false));
+  }
+}
+
 static int dir_blocks(size_t n) {
   size_t b = (n + 255) / 256;
   return int(std::max<size_t>(1, std::min(b, size_t(sm_count()) * 8)));
@@ -719,7 +732,101 @@ static int cast_batch_staged(rl_cddt* c, const float* x, const float* y, const f
   return RL_OK;
 }
 
+// rl_cddt_cast_queries_host: chunks of the RayQuery array go host -> device,
+// through k_cast_queries, and their ranges back, over three streams; pageable
+// arrays (a std::vector<RayQuery>) are staged through pinned buffers by the
+// host threads like cast_batch_staged's.
+static int cast_queries_pipeline(rl_cddt* c, const double* q, double* out, size_t n) {
+  constexpr int NSTREAM = 3;
+  static const int threads = [] {
+    const char* e = std::getenv("RL_HOST_COPY_THREADS");
+    const int hw = int(std::thread::hardware_concurrency());
+    return std::max(1, e ? std::atoi(e) : std::min(8, hw > 1 ? hw / 2 : 1));
+  }();
+  const size_t chunk = std::min(n, size_t(1) << 21);  // 2M queries: 48 MB in, 16 MB out
+  const bool in_direct = dma_direct(q), out_direct = dma_direct(out);
+  struct Lane {
+    cudaStream_t s = nullptr;
+    DevBuf<double> dev;      // 3 x chunk queries | chunk ranges
+    double* pin = nullptr;   // the same layout in page-locked host memory
+    size_t pend_off = 0, pend_m = 0;
+    ~Lane() {
+      if (pin) cudaFreeHost(pin);
+      if (s) cudaStreamDestroy(s);
+    }
+  };
+  static thread_local std::vector<Lane> lanes;
+  static thread_local size_t lane_chunk = 0;
+  static thread_local int lane_dev = -1;
+  if (lanes.empty() || lane_chunk < chunk || lane_dev != c->dev) {
+    lanes.clear();
+    lanes = std::vector<Lane>(NSTREAM);
+    lane_chunk = 0;
+    for (auto& l : lanes) {
+      RL_CK(cudaStreamCreateWithFlags(&l.s, cudaStreamNonBlocking));
+      RL_TRY(l.dev.alloc(4 * chunk));
+      RL_CK(cudaHostAlloc(reinterpret_cast<void**>(&l.pin), 4 * chunk * sizeof(double),
+                          cudaHostAllocDefault));
+    }
+    lane_chunk = chunk;
+    lane_dev = c->dev;
+  }
+  for (auto& l : lanes) l.pend_m = 0;
+  cudaEvent_t ready;
+  RL_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  struct EventGuard {
+    cudaEvent_t e;
+    ~EventGuard() { cudaEventDestroy(e); }
+  } ready_guard{ready};
+  RL_CK(cudaEventRecord(ready, c->stream));  // order after pending structure work
+  const size_t stride = lane_chunk;
+  const CddtView v = c->view();
+  std::vector<CopySeg> segs;
+  size_t k = 0;
+  for (size_t off = 0; off < n; k++) {
+    const size_t m = std::min(n - off, k < 2 ? std::max<size_t>(chunk >> (2 - k), 1) : chunk);
+    Lane& l = lanes[k % NSTREAM];
+    segs.clear();
+    // the lane's pinned block is reused: its previous upload must have left it,
+    // and its previous ranges go to the caller first
+    if (k >= NSTREAM && (!in_direct || l.pend_m)) RL_CK(cudaStreamSynchronize(l.s));
+    if (l.pend_m) {
+      segs.push_back({out + l.pend_off, l.pin + 3 * stride, l.pend_m * sizeof(double)});
+      l.pend_m = 0;
+    }
+    if (!in_direct) segs.push_back({l.pin, q + 3 * off, 3 * m * sizeof(double)});
+    if (!segs.empty()) parallel_copy(segs, threads);
+    RL_CK(cudaStreamWaitEvent(l.s, ready, 0));
+    RL_CK(cudaMemcpyAsync(l.dev.p, in_direct ? q + 3 * off : l.pin, 3 * m * sizeof(double),
+                          cudaMemcpyHostToDevice, l.s));
+    k_cast_queries<<<dir_blocks(m), 256, 0, l.s>>>(v, l.dev.p, l.dev.p + 3 * stride, m);
+    RL_CK(cudaGetLastError());
+    RL_CK(cudaMemcpyAsync(out_direct ? out + off : l.pin + 3 * stride, l.dev.p + 3 * stride,
+                          m * sizeof(double), cudaMemcpyDeviceToHost, l.s));
+    if (!out_direct) {
+      l.pend_off = off;
+      l.pend_m = m;
+    }
+    off += m;
+  }
+  for (size_t j = (k >= NSTREAM ? k - NSTREAM : 0); j < k; j++) {  // drain in submission order
+    Lane& l = lanes[j % NSTREAM];
+    RL_CK(cudaStreamSynchronize(l.s));
+    if (!l.pend_m) continue;
+    parallel_copy({{out + l.pend_off, l.pin + 3 * stride, l.pend_m * sizeof(double)}}, threads);
+    l.pend_m = 0;
+  }
+  return RL_OK;
+}
+
 extern "C" {
+
+int rl_cddt_cast_queries_host(rl_cddt* c, const double* queries, double* out, size_t n) {
+  if (!c || (n && (!queries || !out))) return RL_EINVAL;
+  if (n == 0) return RL_OK;
+  DeviceGuard guard(c->dev);
+  return cast_queries_pipeline(c, queries, out, n);
+}
 
 // One query (Cddt::cast / cast_pair): a one-thread kernel that writes its
 // answer straight into the handle's pinned host words (device-visible under

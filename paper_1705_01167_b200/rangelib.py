@@ -355,6 +355,20 @@ class Cddt:
                                        _ptr(hit), n, s))
         return out
 
+    def cast_queries(self, queries, out=None):
+        """The per-query loop of run_batches (bench.cpp:86-106) over an [n, 3] float64
+        array of RayQuery rows (x, y, theta) in host memory; returns float64 ranges."""
+        q = np.ascontiguousarray(queries, dtype=np.float64)
+        if q.ndim != 2 or q.shape[1] != 3:
+            raise ValueError("queries must be an [n, 3] array of (x, y, theta)")
+        res = np.empty(q.shape[0], dtype=np.float64) if out is None else out
+        if not (isinstance(res, np.ndarray) and res.dtype == np.float64
+                and res.flags.c_contiguous and res.flags.writeable and res.size == q.shape[0]):
+            raise ValueError("out must be a writable contiguous float64 array of len(queries)")
+        check(lib().rl_cddt_cast_queries_host(self._h, q.ctypes.data, res.ctypes.data,
+                                              q.shape[0]))
+        return res
+
     def cast_batch_f64(self, x, y, theta, out=None, hit=None, res_row=None, res_idx=None,
                        stream=None):
         import torch

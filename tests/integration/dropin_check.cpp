@@ -420,6 +420,26 @@ int main() {
     }
     report("invalid_argument / logic_error mapping", ok && ok2, 0);
   }
+  // 5. run_batches' inner loop (proj/src/bench.cpp:86-106) over a std::vector<RayQuery>,
+  //    as one cast_many call: ranges bit-identical to the reference's cast loop
+  {
+    OccupancyGrid g = make_random_map(96, 80, 0.07, 21);
+    RangeMethodConfig cfg;
+    long diff = 0;
+    for (bool prune : {false, true}) {
+      auto ref = make_method(prune ? MethodKind::pcddt : MethodKind::cddt, g, cfg);
+      rl_gpu::GpuCddtMethod gpu(g, cfg, prune);
+      SplitMix64 rng(123);
+      std::vector<RayQuery> buf;
+      for (int i = 0; i < 200000; i++)
+        buf.emplace_back(rng.uniform(-1.0, 97.0), rng.uniform(-1.0, 81.0), rng.uniform(-7.0, 7.0));
+      std::vector<double> out(buf.size());
+      gpu.cast_many(buf.data(), buf.size(), out.data());
+      for (size_t i = 0; i < buf.size(); i++) diff += ref->cast(buf[i]) != out[i];
+    }
+    report("cast_many(std::vector<RayQuery>) bit-identical to the reference's cast loop", diff == 0,
+           diff);
+  }
   acceptance_2();
   acceptance_3();
   acceptance_4();

@@ -847,3 +847,41 @@ def test_host_path_pageable_pinned_and_mixed(rl, synth):
         out2 = np.zeros(n, dtype=np.float32)
         gpu.cast_batch(pin[0][:n], qy[:n], pin[2][:n], out=out2)  # mixed
         assert np.array_equal(out2.view(np.uint32), want[:n].view(np.uint32)), n
+
+
+def test_cast_queries_host_rayquery_array(rl, oracle_mod, synth):
+    """rl_cddt_cast_queries_host: an [n, 3] array of RayQuery rows (doubles, not
+    float-representable) from pageable and pinned host memory equals the f64
+    device path bit for bit, at sizes around the pipeline's chunks, and the
+    reference / restatement on a sample."""
+    import torch
+    g = synth.rect_map(300, 260, 14, seed=4)
+    gpu = make_gpu(rl, g, 108, 200.0)
+    nmax = (5 << 20) + 777
+    qx, qy, qt = synth.free_queries(g, nmax, seed=23)
+    rng = np.random.default_rng(6)
+    q = np.stack([qx.astype(np.float64) + rng.uniform(-1e-4, 1e-4, nmax),
+                  qy.astype(np.float64) + rng.uniform(-1e-4, 1e-4, nmax),
+                  qt.astype(np.float64) * 3.0 - 4.0 + rng.uniform(-1e-6, 1e-6, nmax)], axis=1)
+    want = host(gpu.cast_batch_f64(dev(q[:, 0]), dev(q[:, 1]), dev(q[:, 2])))
+    torch.cuda.synchronize()
+    qp = torch.from_numpy(q).pin_memory().numpy()
+    for n in (nmax, 2 << 20, (1 << 19) + 1, 3, 0):
+        got = gpu.cast_queries(q[:n])  # pageable in and out
+        assert np.array_equal(got.view(np.uint64), want[:n].view(np.uint64)), n
+        out = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+        gpu.cast_queries(qp[:n], out=out)  # pinned in and out
+        assert np.array_equal(out.view(np.uint64), want[:n].view(np.uint64)), n
+        out2 = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+        gpu.cast_queries(q[:n], out=out2)  # pageable in, pinned out
+        assert np.array_equal(out2.view(np.uint64), want[:n].view(np.uint64)), n
+    m = 20_000
+    if oracle_mod.ref_available():
+        ref, _ = oracle_mod.RefCddt(g, 108, 200.0).cast_pair_batch(q[:m, 0], q[:m, 1], q[:m, 2])
+    else:
+        o = oracle_mod.OracleCddt(g, 108, 200.0)
+        m = 2_000
+        ref = np.array([o.cast(*q[i]) for i in range(m)])
+    assert np.array_equal(want[:m].view(np.uint64), np.asarray(ref).view(np.uint64))
+    with pytest.raises(ValueError):
+        gpu.cast_queries(np.zeros((4, 2)))
