@@ -577,7 +577,6 @@ def cpu_model():
 
 # ---------------------------------------------------------------- arms
 def run_ours(args, rank, world, local_rank):
-    import numpy as np
     import torch
     import torch.distributed as dist
 

@@ -352,10 +352,20 @@ static void launch_k_cast(const CddtView& v, const T* x, const T* y, const T* t,
   k_cast<T, I, HIT, RES><<<int(b), 256, 0, st>>>(v, x, y, t, out, hit, rr, ri, I(n));
 }
 
-#ifndef RL_DEFER_MIN_LOG2
-#define RL_DEFER_MIN_LOG2 22
-#endif
-constexpr size_t kDeferMinQueries = size_t(1) << RL_DEFER_MIN_LOG2;
+// Batch-size plan of the range-only f32 cast (measured on B200, configs 2 and 3):
+//   n <  kDeferMinQueries   single kernel (the split pipeline's six dependent launches cost more)
+//   n >= kDeferMinQueries   split pipeline; with window caps {2} (one capped pass, then the
+//                           finishing pass) while a pipeline holds fewer than kShortPlanMax
+//                           queries, {1, 2, 4} above
+//   n >= kTwoPipeMin        two pipelines over the halves of the batch
+// RL_DEFER_MIN / RL_TWO_PIPE_MIN / RL_SHORT_PLAN_MAX (environment) override them for A/B runs.
+static size_t env_size(const char* name, size_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? size_t(std::strtoull(e, nullptr, 10)) : dflt;
+}
+static const size_t kDeferMinQueries = env_size("RL_DEFER_MIN", size_t(5) << 18);   // 1.31M
+static const size_t kTwoPipeMin = env_size("RL_TWO_PIPE_MIN", size_t(1) << 22);     // 4.2M
+static const size_t kShortPlanMax = env_size("RL_SHORT_PLAN_MAX", size_t(1) << 23);  // per pipeline
 
 // Dispatch of the batched cast kernels for the device-pointer entry points.
 template <class T>
@@ -383,7 +393,8 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
   // the split pipeline's records hold the query as floats: f32 batches only
   // (f64 queries need not be float-representable; they take k_cast)
   constexpr bool kF32 = std::is_same<T, float>::value;
-  if (kF32 && split && parts > 1 && !rr && !ri && !hit && small && n >= kDeferMinQueries * parts) {
+  if (kF32 && split && parts > 1 && !rr && !ri && !hit && small && n >= kTwoPipeMin &&
+      n >= kDeferMinQueries * parts) {
     // two independent pipelines over the halves of the batch, on the caller's
     // stream and a forked one: the late, thinly occupied window passes of one
     // overlap the other's phase 1
@@ -423,15 +434,13 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
       const char* e = std::getenv("RL_CDDT_CONT_CAP");
       return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(0);
     }();
-#ifdef RL_WIN_CAPS_CODE  // A/B builds: decimal digits, e.g. 1124 -> {1, 1, 2, 4}
-    constexpr int kPasses = RL_WIN_CAPS_CODE >= 1000 ? 4 : RL_WIN_CAPS_CODE >= 100 ? 3
-                                                     : RL_WIN_CAPS_CODE >= 10 ? 2 : 1;
-    int kCaps[kPasses];
-    for (int p = kPasses - 1, v = RL_WIN_CAPS_CODE; p >= 0; p--, v /= 10) kCaps[p] = v % 10;
-#else
-    constexpr int kCaps[] = {RL_WIN_CAPS};
-    constexpr int kPasses = sizeof(kCaps) / sizeof(kCaps[0]);  // capped passes; one more runs out
-#endif
+    // capped window passes of this pipeline; one more pass finishes
+    static constexpr int kCapsFull[] = {RL_WIN_CAPS}, kCapsShort[] = {2};
+    const bool short_plan = n < kShortPlanMax;
+    const int* kCaps = short_plan ? kCapsShort : kCapsFull;
+    const int kPasses = short_plan ? int(sizeof(kCapsShort) / sizeof(int))
+                                   : int(sizeof(kCapsFull) / sizeof(int));
+    constexpr int kMaxPasses = int(sizeof(kCapsFull) / sizeof(int));
     const size_t cap_a = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_A_DIV, size_t(1) << 16);
     const size_t cap_b = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_B_DIV, size_t(1) << 16);
     uint8_t* ws = nullptr;
@@ -456,7 +465,7 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
     static const int pwc = walk_ctas(k_walk_pass<T, true, false>);
     static const int pwl = walk_ctas(k_walk_pass<T, true, true>);
     static const int pn = walk_ctas(k_cast_near<T>);
-    RL_CK(cudaMemsetAsync(qn, 0, (2 + kPasses) * sizeof(unsigned), st));
+    RL_CK(cudaMemsetAsync(qn, 0, (2 + kMaxPasses) * sizeof(unsigned), st));
     const size_t b1 = std::max<size_t>(
         1, std::min((n + kP1Threads - 1) / kP1Threads, size_t(sm_count()) * p1));
     k_cast_defer_p1<T><<<int(b1), kP1Threads, 0, st>>>(v, x, y, t, out, uint32_t(n), q, qn);
@@ -495,8 +504,8 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
         nullptr, 0, out);
 #ifdef RL_DEBUG_COUNTS
     {
-      unsigned h[2 + kPasses];
-      cudaMemcpyAsync(h, qn, sizeof h, cudaMemcpyDeviceToHost, st);
+      unsigned h[2 + kMaxPasses];
+      cudaMemcpyAsync(h, qn, (2 + kPasses) * sizeof(unsigned), cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       fprintf(stderr, "counts n=%zu windows=%u near=%u", n, h[0], h[1]);
       for (int p = 0; p < kPasses; p++) fprintf(stderr, " after pass %d: %u", p, h[2 + p]);

@@ -636,11 +636,16 @@ print("EQUAL" if torch.equal(split, whole.float()) else "DIFFER")
 """
 
 
-@pytest.mark.parametrize("cap", ["", "4096", "1"])
-def test_window_pass_queues(cap):
+@pytest.mark.parametrize("cap,plan", [("", ""), ("4096", ""), ("1", ""), ("", "full"),
+                                      ("1", "full"), ("", "one"), ("", "short-one")])
+def test_window_pass_queues(cap, plan):
     """The window passes hand unfinished queries on through bounded queues;
     with the queue capacity forced tiny (RL_CDDT_CONT_CAP) nearly every
-    continuation takes the queue-full path, which must give the same answers."""
+    continuation takes the queue-full path, which must give the same answers.
+    The batch-size plan is forced too: by default 8M queries run as two
+    pipelines with the short window plan {2}; "full" forces caps {1, 2, 4},
+    "one" a single pipeline with the full plan, "short-one" a single pipeline
+    with the short plan."""
     import os
     import subprocess
     import sys
@@ -648,6 +653,10 @@ def test_window_pass_queues(cap):
     env = dict(os.environ)
     if cap:
         env["RL_CDDT_CONT_CAP"] = cap
+    if plan in ("full", "one"):
+        env["RL_SHORT_PLAN_MAX"] = "0"
+    if plan in ("one", "short-one"):
+        env["RL_TWO_PIPE_MIN"] = "1000000000"
     root = str(Path(__file__).resolve().parent.parent)
     r = subprocess.run([sys.executable, "-c", _QUEUE_CHECK.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
