@@ -277,6 +277,64 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinCtas) k_walk_pass(
   }
 }
 
+// The finishing pass, warp-cooperative. What reaches it are the rays grazing
+// walls: few records, but chains of tens to hundreds of verification windows,
+// so a lane-per-record pass lasts as long as its longest chain (45 us whether
+// the batch has 1M or 50M queries). Each lane first scans up to `cap` more
+// windows of its own record; a record still unfinished is then taken by the
+// whole warp, 32 candidates at a time (resume_coop: every candidate's verdict
+// is a pure function of the candidate, the first non-clean one in candidate
+// order decides, exactly as the sequential loop does).
+#ifndef RL_LAST_COOP
+#define RL_LAST_COOP 1
+#endif
+#ifndef RL_LAST_COOP_CAP
+#define RL_LAST_COOP_CAP 8  // 0 / 2 / 4: slower (whole warps spent on short chains); 12-40: equal to slower
+#endif
+template <class T>
+__global__ void __launch_bounds__(kWalkThreads, kWalkMinCtas) k_walk_last_coop(
+    CddtView c, const ContRecord* __restrict__ in, const unsigned* __restrict__ in_count,
+    uint32_t in_cap, int cap, T* __restrict__ out) {
+  const unsigned m = min(*in_count, in_cap);
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned warps = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned b0 = warp * 32u; b0 < m; b0 += warps * 32u) {
+    const unsigned k = b0 + lane;
+    bool open = false;
+    float fx = 0.f, fy = 0.f;
+    uint32_t qi = 0;
+    WinState s{};
+    int a = 0;
+    if (k < m) {
+      const float4* src = reinterpret_cast<const float4*>(in + k);
+      const float4 w0 = __ldcs(src), w1 = __ldcs(src + 1), w2 = __ldcs(src + 2);
+      fx = w0.x;
+      fy = w0.y;
+      qi = __float_as_uint(w0.w);
+      s = WinState{__float_as_uint(w1.x), __float_as_uint(w1.y), __float_as_int(w1.z),
+                   __float_as_int(w1.w), __float_as_int(w2.x),
+                   __hiloint2double(__float_as_int(w2.w), __float_as_int(w2.z)), 0.f};
+      a = __float_as_int(w2.y);
+      double res;
+      if (resume_windows<false>(c, double(fx), double(fy), a, s, cap, &res))
+        __stcs(out + qi, T(res));
+      else
+        open = true;
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, open);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const float x = __shfl_sync(0xffffffffu, fx, j), y = __shfl_sync(0xffffffffu, fy, j);
+      const int aj = __shfl_sync(0xffffffffu, a, j), ij = __shfl_sync(0xffffffffu, s.idx, j);
+      const uint32_t oj = __shfl_sync(0xffffffffu, qi, j);
+      const double r = resume_coop(c, double(x), double(y), aj, ij);
+      if (lane == 0) __stcs(out + oj, T(r));
+    }
+  }
+}
+
 // Near-field records (origin not clear): near-field walk, search and landing
 // probes here; queries that need a verification window join the window
 // passes as continuations (queue A, after pass 0's own).
@@ -363,7 +421,7 @@ static size_t env_size(const char* name, size_t dflt) {
   const char* e = std::getenv(name);
   return e ? size_t(std::strtoull(e, nullptr, 10)) : dflt;
 }
-static const size_t kDeferMinQueries = env_size("RL_DEFER_MIN", size_t(5) << 18);   // 1.31M
+static const size_t kDeferMinQueries = env_size("RL_DEFER_MIN", size_t(3) << 18);   // 786k
 static const size_t kTwoPipeMin = env_size("RL_TWO_PIPE_MIN", size_t(1) << 22);     // 4.2M
 static const size_t kShortPlanMax = env_size("RL_SHORT_PLAN_MAX", size_t(1) << 23);  // per pipeline
 
@@ -499,9 +557,16 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
           from_a ? qb : qa, qn + 2 + p, uint32_t(from_a ? cap_b : cap_a), out);
     }
     const bool last_a = (kPasses & 1) != 0;
+#if RL_LAST_COOP
+    static const int pwk = walk_ctas(k_walk_last_coop<T>);
+    k_walk_last_coop<T><<<sm_count() * pwk, kWalkThreads, 0, st>>>(
+        v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b),
+        RL_LAST_COOP_CAP, out);
+#else
     k_walk_pass<T, true, true><<<sm_count() * pwl, kWalkThreads, 0, st>>>(
         v, last_a ? qa : qb, qn + 1 + kPasses, uint32_t(last_a ? cap_a : cap_b), 0, nullptr,
         nullptr, 0, out);
+#endif
 #ifdef RL_DEBUG_COUNTS
     {
       unsigned h[2 + kMaxPasses];
