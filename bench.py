@@ -708,7 +708,7 @@ def run_ours(args, rank, world, local_rank):
                     "path": "rl_cddt_cast_batch_host (pinned host buffers, 3-stream pipeline)",
                     "pageable": e2e_pageable},
             # per step: two pipelines (one per half of the batch) of k_cast_defer_p1,
-            # k_cast_near and four k_walk_pass window passes
+            # k_cast_near and three capped k_walk_pass window passes and the k_walk_last_coop finishing pass
             "gpu_launches": 12 * args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -718,7 +718,7 @@ def run_ours(args, rank, world, local_rank):
                          "traffic_source": (tr or {}).get("source"),
                          "sector_sample": ns,
                          "kernel": "batched cast = 2 pipelines (halves of the batch, two streams) of "
-                                   "k_cast_defer_p1 + k_cast_near + 4 x k_walk_pass (window passes); "
+                                   "k_cast_defer_p1 + k_cast_near + 3 x k_walk_pass (capped window passes) + k_walk_last_coop (finishing pass); "
                                    "timed per step",
                          "gather_ceiling": gather},
             "cpu_baseline": {"value": sample / ref_dt, "unit": UNIT, "cores": threads,
