@@ -394,68 +394,6 @@ __global__ void __launch_bounds__(kWalkThreads, kWalkMinCtas) k_cast_near(
   }
 }
 
-// Small range-only f32 batches (below the split pipeline's minimum): the single
-// kernel with a cap on the verification windows a thread scans, and a second
-// launch in which whole warps finish the few casts that ran into it (rays
-// grazing walls, whose chains of windows otherwise decide the kernel time).
-struct __align__(16) LongRecord {
-  float x, y;
-  int32_t a, idx;   // direction index, next candidate
-  uint32_t i, pad0, pad1, pad2;
-};
-
-// out-of-line: the rare queue-full path must not add to the kernel's registers
-__device__ __noinline__ double cast_uncapped(const CddtView& c, double x, double y, int a) {
-  double r;
-  int next;
-  directional_cast_capped(c, x, y, a, -1, &r, &next);
-  return r;
-}
-
-#ifndef RL_CAPPED_MINB
-#define RL_CAPPED_MINB 4
-#endif
-__global__ void __launch_bounds__(256, RL_CAPPED_MINB) k_cast_capped(
-    CddtView c, const float* __restrict__ qx, const float* __restrict__ qy,
-    const float* __restrict__ qt, float* __restrict__ out, uint32_t n, int cap,
-    LongRecord* __restrict__ lq, unsigned* __restrict__ lq_n, uint32_t lq_cap) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const float fx = __ldcs(qx + i), fy = __ldcs(qy + i);
-    const double th = normalize_angle_2pi(double(__ldcs(qt + i)));
-    const int a = direction_index(th, c.K);
-    double r;
-    int next = 0;
-    if (!directional_cast_capped(c, double(fx), double(fy), a, cap, &r, &next)) {
-      const unsigned slot = atomicAdd(lq_n, 1u);
-      if (slot < lq_cap) {
-        float4* dst = reinterpret_cast<float4*>(lq + slot);
-        dst[0] = make_float4(fx, fy, __int_as_float(a), __int_as_float(next));
-        dst[1] = make_float4(__uint_as_float(i), 0.f, 0.f, 0.f);
-        continue;
-      }
-      r = cast_uncapped(c, double(fx), double(fy), a);  // queue full
-    }
-    __stcs(out + i, float(r));
-  }
-}
-
-__global__ void __launch_bounds__(256) k_finish_coop(CddtView c, const LongRecord* __restrict__ lq,
-                                                     const unsigned* __restrict__ lq_n,
-                                                     uint32_t lq_cap, float* __restrict__ out) {
-  const unsigned m = min(*lq_n, lq_cap);
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned warps = (gridDim.x * blockDim.x) >> 5;
-  for (unsigned k = warp; k < m; k += warps) {
-    const float4* src = reinterpret_cast<const float4*>(lq + k);
-    const float4 w0 = __ldg(src);
-    const uint32_t i = __float_as_uint(__ldg(reinterpret_cast<const float*>(src + 1)));
-    const double r = resume_coop(c, double(w0.x), double(w0.y), __float_as_int(w0.z),
-                                 __float_as_int(w0.w));
-    if (lane == 0) __stcs(out + i, float(r));
-  }
-}
-
 // CTAs per SM for a kernel at 256 threads (one full wave, no partial tail).
 template <class K>
 static int resident_ctas(K kernel) {
@@ -641,25 +579,6 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
 #endif
     RL_TRY(scratch_free(ws, st));
     return RL_OK;
-  }
-  if constexpr (kF32) {
-    static const size_t coop_min = env_size("RL_CAPPED_MIN", size_t(1) << 62);
-    if (!rr && !ri && !hit && small && n >= coop_min) {
-      static const int cap = int(env_size("RL_CAPPED_WINDOWS", 8));
-      const size_t lq_cap = std::max<size_t>(n / 16, 4096);
-      uint8_t* ws = nullptr;
-      RL_TRY(scratch_alloc(reinterpret_cast<void**>(&ws), 256 + sizeof(LongRecord) * lq_cap, st));
-      unsigned* lq_n = reinterpret_cast<unsigned*>(ws);
-      LongRecord* lq = reinterpret_cast<LongRecord*>(ws + 256);
-      RL_CK(cudaMemsetAsync(lq_n, 0, sizeof(unsigned), st));
-      static const int per_sm = resident_ctas(k_cast_capped);
-      const size_t b = std::max<size_t>(1, std::min((n + 255) / 256, size_t(sm_count()) * per_sm));
-      k_cast_capped<<<int(b), 256, 0, st>>>(v, x, y, t, out, uint32_t(n), cap, lq, lq_n,
-                                            uint32_t(lq_cap));
-      k_finish_coop<<<sm_count() * 2, 256, 0, st>>>(v, lq, lq_n, uint32_t(lq_cap), out);
-      RL_TRY(scratch_free(ws, st));
-      return RL_OK;
-    }
   }
   if (rr || ri) {
     launch_k_cast<T, size_t, true, true>(v, x, y, t, out, hit, rr, ri, n, st);
