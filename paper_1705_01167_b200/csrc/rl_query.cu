@@ -493,12 +493,23 @@ static int launch_cast(const rl_cddt* c, const T* x, const T* y, const T* t, T* 
       return e ? size_t(std::strtoull(e, nullptr, 10)) : size_t(0);
     }();
     // capped window passes of this pipeline; one more pass finishes
-    static constexpr int kCapsFull[] = {RL_WIN_CAPS}, kCapsShort[] = {2};
+    // (RL_WIN_CAPS_ENV / RL_SHORT_CAPS_ENV: decimal digits, e.g. 124 -> {1, 2, 4}, for A/B runs)
+    struct Caps {
+      int n = 0, v[4] = {0, 0, 0, 0};
+      Caps(const char* name, std::initializer_list<int> dflt) {
+        const char* e = std::getenv(name);
+        if (e && *e) {
+          for (const char* q = e; *q && n < 4; q++) v[n++] = *q - '0';
+        } else {
+          for (int d : dflt) v[n++] = d;
+        }
+      }
+    };
+    static const Caps caps_full("RL_WIN_CAPS_ENV", {RL_WIN_CAPS}), caps_short("RL_SHORT_CAPS_ENV", {2});
     const bool short_plan = n < kShortPlanMax;
-    const int* kCaps = short_plan ? kCapsShort : kCapsFull;
-    const int kPasses = short_plan ? int(sizeof(kCapsShort) / sizeof(int))
-                                   : int(sizeof(kCapsFull) / sizeof(int));
-    constexpr int kMaxPasses = int(sizeof(kCapsFull) / sizeof(int));
+    const int* kCaps = short_plan ? caps_short.v : caps_full.v;
+    const int kPasses = short_plan ? caps_short.n : caps_full.n;
+    constexpr int kMaxPasses = 4;
     const size_t cap_a = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_A_DIV, size_t(1) << 16);
     const size_t cap_b = cap_env ? cap_env : std::max<size_t>(n / RL_CONT_B_DIV, size_t(1) << 16);
     uint8_t* ws = nullptr;
