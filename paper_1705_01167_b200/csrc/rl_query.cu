@@ -19,7 +19,7 @@ namespace rl {
 // K3: batched casts.
 //
 // Monolithic form (f64 / hit-cell / resolving-index outputs, and batches
-// below 4M queries): one thread per query, grid-stride, a single full wave
+// below kDeferMinQueries, 786k): one thread per query, grid-stride, a single full wave
 // sized by the occupancy calculator (4 x 256-thread CTAs per SM at 64 regs).
 template <class T, class I, bool HIT, bool RES>
 __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict__ qx,
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256, 4) k_cast(CddtView c, const T* __restrict
   }
 }
 
-// Deferred-walk form (f32 ranges only, >= 4M queries; the bench path).
+// Deferred-walk form (f32 ranges only, >= kDeferMinQueries; the bench path).
 // About a third of the queries need a RayWalker (a near-field walk or a
 // verification window). Run inline, those walks execute with ~5 of 32 lanes
 // active and cost half the kernel time (profiles/r01/ncu_k_cast_v3.txt).
@@ -735,7 +735,7 @@ static int cast_batch_staged(rl_cddt* c, const float* x, const float* y, const f
   }();
   static const size_t chunk_max = [] {
     const char* e = std::getenv("RL_HOST_STAGE_CHUNK_LOG2");
-    return size_t(1) << (e ? std::atoi(e) : 22);  // 4M queries: the split pipeline's minimum
+    return size_t(1) << (e ? std::atoi(e) : 22);  // 4M queries (two pipelines of 2M each)
   }();
   const size_t chunk = std::min(n, chunk_max);
   struct Lane {
